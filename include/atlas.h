@@ -1,0 +1,221 @@
+/*
+ * atlas.h -- C-ABI of the B200-native Atlas hot path (arXiv 2408.09055).
+ *
+ * The library simulates a quantum circuit on a 2^n complex state vector that
+ * is sharded over `world` B200 GPUs (one process per GPU), following the
+ * paper's problem statement
+ *     Simulate(C, state, L, R, G)          PAPER.md P:L1321-1324 (Alg. 1)
+ *     = Execute(Partition(C, L, R, G), state)
+ * with the physical-qubit hierarchy collapsed onto one 8xB200 NVSwitch box:
+ * L = n - log2(world) local qubits (each GPU's HBM shard, Def. P:L1405-1417),
+ * R = 0 regional qubits, G = log2(world) global qubits (the rank bits).
+ *
+ *   atlas_create       Simulate's machine parameters (n, L, R=0, G)
+ *   atlas_load_circuit C, a gate sequence
+ *   atlas_plan         Partition: Stage (ILP) + Kernelize per
+ *                      stage (App. P:L2348-2499) + lowering
+ *   atlas_run          Execute: per stage, Shard (remap
+ *                      all-to-all) then LaunchKernel for each kernel
+ *   atlas_get_state    read amplitudes back in logical order
+ *
+ * Conventions:
+ *  - Amplitude index: logical qubit q is bit q of the index (Eq. 2).
+ *  - Gate operands: q[0] is the least-significant bit of the gate's matrix
+ *    index.  Controlled kinds list controls first: CX(c,t), CP(c,t), CU(c,t),
+ *    CCX(c0,c1,t).  Matrices are the textbook / OpenQASM ones (R2).
+ *  - Amplitudes are interleaved (re, im): double2 for ATLAS_C128, float2 for
+ *    ATLAS_C64, little endian.
+ *
+ * Ownership: the context owns the plan and (unless atlas_bind_buffers is
+ * used) all device memory.  Gate arrays and host buffers are caller-owned
+ * and only read/written during the call.  No call retains a caller pointer
+ * except atlas_bind_buffers / atlas_set_stream (borrowed until destroy or
+ * rebinding).
+ *
+ * Errors: every call returns an atlas_status; no exception crosses the ABI.
+ * atlas_last_error() returns a thread-local message for the last failure.
+ * Device work only starts in atlas_run / atlas_get_state / atlas_set_state;
+ * create/load/plan are host-only (usable without a GPU for planning).
+ *
+ * Threading: a context is not thread-safe; use one context per thread.
+ */
+#ifndef ATLAS_H_
+#define ATLAS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct atlas_ctx atlas_ctx;
+
+typedef enum {
+  ATLAS_C128 = 0, /* complex128: 2 x fp64 per amplitude (P:L1964 footnote) */
+  ATLAS_C64 = 1   /* complex64: 2 x fp32 per amplitude                     */
+} atlas_dtype;
+
+typedef enum {
+  ATLAS_OK = 0,
+  ATLAS_E_INVALID = 1,     /* bad argument: n<1, world not a power of 2,
+                              G>n, qubit out of range, duplicate operand     */
+  ATLAS_E_UNSUPPORTED = 2, /* unknown gate kind / option                     */
+  ATLAS_E_INFEASIBLE = 3,  /* a gate has more non-insular qubits than L, or
+                              no staging within s_max (P:L1526 loop)         */
+  ATLAS_E_BUDGET = 4,      /* search budget exceeded                         */
+  ATLAS_E_OOM = 5,         /* device/host allocation failed                  */
+  ATLAS_E_CUDA = 6,        /* CUDA runtime error (or no CUDA device)         */
+  ATLAS_E_NCCL = 7,        /* NCCL error / library not loadable              */
+  ATLAS_E_ORDER = 8        /* call order violated (run before plan, ...)     */
+} atlas_status;
+
+/* Gate kinds.  Parameters p[] in radians. */
+enum {
+  ATLAS_GATE_H = 0, ATLAS_GATE_X = 1, ATLAS_GATE_Y = 2, ATLAS_GATE_Z = 3,
+  ATLAS_GATE_S = 4, ATLAS_GATE_SDG = 5, ATLAS_GATE_T = 6, ATLAS_GATE_TDG = 7,
+  ATLAS_GATE_RX = 8,   /* p0 = theta                                      */
+  ATLAS_GATE_RY = 9,   /* p0 = theta                                      */
+  ATLAS_GATE_RZ = 10,  /* p0 = theta: diag(e^{-i t/2}, e^{i t/2})          */
+  ATLAS_GATE_P = 11,   /* p0 = lambda: diag(1, e^{i l})                    */
+  ATLAS_GATE_U3 = 12,  /* p0..2 = theta, phi, lambda                       */
+  ATLAS_GATE_CX = 13, ATLAS_GATE_CZ = 14,
+  ATLAS_GATE_CP = 15,  /* p0 = lambda                                      */
+  ATLAS_GATE_CCX = 16, ATLAS_GATE_SWAP = 17,
+  ATLAS_GATE_CU = 18,  /* OpenQASM 3 cu(theta, phi, lambda, gamma)         */
+  ATLAS_GATE_NKINDS = 19
+};
+
+/* One gate.  nq must equal the kind's arity; q[nq..2] and unused p[] are
+ * ignored.  48 bytes, naturally aligned. */
+typedef struct {
+  uint32_t kind;
+  uint32_t nq;
+  uint32_t q[3];
+  uint32_t pad_;
+  double p[4];
+} atlas_gate;
+
+/* ---------------------------------------------------------------- core */
+
+/* Create a context for an n-qubit state sharded over `world` ranks (a power
+ * of two, 1..64); this process is `rank`.  G = log2(world) global qubits,
+ * L = n - G local qubits, R = 0.
+ * nccl_uid: 128-byte ncclUniqueId from atlas_nccl_unique_id() on rank 0,
+ * broadcast to all ranks; NULL when world == 1 or in virtual-world mode
+ * (option "virtual_world": all ranks' shards live on this process's GPU,
+ * the remap runs as device copies -- used to test W>1 plans on one GPU).
+ * Host-only: no CUDA call is made here.  *out receives the context. */
+atlas_status atlas_create(int n, atlas_dtype dtype, int world, int rank,
+                          const void *nccl_uid, atlas_ctx **out);
+
+/* Copy m gates (caller keeps ownership).  Validates kinds, arity, range and
+ * distinctness.  Invalidates any existing plan. */
+atlas_status atlas_load_circuit(atlas_ctx *ctx, const atlas_gate *gates, size_t m);
+
+/* Partition: Stage with at most s_max stages and inter-node
+ * cost factor c (Eq. P:L1477; c = 3 in the paper), then Kernelize
+ * each stage with the cost model, then lower to device programs.
+ * Deterministic: every rank computes the same plan.  Host-only. */
+atlas_status atlas_plan(atlas_ctx *ctx, int s_max, double c);
+
+/* Execute on this rank's GPU: initialise |0...0> (unless the
+ * option "init" is 0, in which case the state written by atlas_set_state is
+ * used), then for every stage: remap (if not the first) and launch its
+ * kernels.  Blocks until the work on the context's stream is complete.
+ * The first call allocates device memory (2^L amplitudes + an equal scratch
+ * buffer when world > 1, times world in virtual-world mode). */
+atlas_status atlas_run(atlas_ctx *ctx);
+
+/* Copy amplitudes [first, first+count) of the final state, in LOGICAL index
+ * order, into host_buf (count amplitudes of the context's dtype).  With
+ * world > 1 (real NCCL ranks) each rank writes only the entries its shard
+ * holds and leaves the others untouched; in virtual-world mode and world==1
+ * every entry is written. */
+atlas_status atlas_get_state(atlas_ctx *ctx, void *host_buf, uint64_t first,
+                             uint64_t count);
+
+/* Write amplitudes [first, first+count) (logical order) of the INITIAL state
+ * of the next atlas_run (requires a plan: the stage-0 placement decides where
+ * they go).  Use with option "init" = 0.  Entries not owned by this rank are
+ * ignored.  The simulation works for arbitrary input states. */
+atlas_status atlas_set_state(atlas_ctx *ctx, const void *host_buf, uint64_t first,
+                             uint64_t count);
+
+void atlas_destroy(atlas_ctx *ctx);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *atlas_last_error(void);
+
+/* ------------------------------------------------------------- options */
+/* Integer options (defaults in brackets):
+ *   "kernelizer"     0 = Kernelize DP [0], 1 = OrderedKernelize
+ *                    (P:L2354), 2 = greedy fusion packing up to 5 qubits
+ *                    (the paper's baseline)
+ *   "prune_T"        Kernelize pruning threshold T [500];
+ *                    <= 0 means no pruning
+ *   "ls_qubits"      least-significant physical qubits forced into every
+ *                    shared-memory kernel (P:L1964 footnote: 3) [5]
+ *   "shm_qubits"     override q_max_shared of the cost model [model]
+ *   "fusion_qubits"  override q_max_fusion of the cost model [model]
+ *   "kinds"          bit 0 fusion, bit 1 shared-memory [3]
+ *   "insular_lift"   Kernelize insular-qubit relaxation [1]
+ *   "attach"         Kernelize single-qubit attachment [1]
+ *   "virtual_world"  1 = all ranks on this GPU (see atlas_create) [0]
+ *   "init"           1 = atlas_run starts from |0...0> [1]
+ *   "timing"         1 = per-launch CUDA events (atlas_get_launches) [0]
+ *   "device"         CUDA device ordinal [current device]
+ *   "stage_budget"   staging search state budget [2000000]
+ * String options:
+ *   "cost_model"     path of a cost-model JSON (SPEC S:L358 format, integer
+ *                    units); default: the built-in B200 fp64/fp32 model
+ * Return ATLAS_E_UNSUPPORTED for unknown keys. */
+atlas_status atlas_set_option_int(atlas_ctx *ctx, const char *key, int64_t value);
+atlas_status atlas_set_option_str(atlas_ctx *ctx, const char *key, const char *value);
+
+/* --------------------------------------------------------- plumbing */
+
+/* Borrow device buffers owned by the caller (e.g. PyTorch tensors): `state`
+ * and `scratch` each of `bytes` >= 2^L * sizeof(amplitude) (x world in
+ * virtual-world mode); scratch may be NULL when world == 1. */
+atlas_status atlas_bind_buffers(atlas_ctx *ctx, void *state, void *scratch,
+                                uint64_t bytes);
+
+/* Run on the given cudaStream_t (borrowed; NULL = the context's own stream). */
+atlas_status atlas_set_stream(atlas_ctx *ctx, void *cuda_stream);
+
+/* 128-byte ncclUniqueId for atlas_create (rank 0 calls it, then broadcasts).
+ * Loads libnccl.so.2 at run time. */
+atlas_status atlas_nccl_unique_id(void *out128);
+
+/* ---------------------------------------------------------- reports */
+
+/* The plan as JSON (stages with local/global logical sets, gate->stage map,
+ * physical placement, per-stage kernels {gates, kind, qubits, cost}, totals).
+ * Writes at most cap bytes (NUL-terminated when it fits); *len receives the
+ * full length (call with cap = 0 to size). */
+atlas_status atlas_get_plan_json(atlas_ctx *ctx, char *buf, size_t cap, size_t *len);
+
+/* Plan summary, int64 values in this order (count = min(cap, 12)):
+ *   0 stages  1 staging cost x1000  2 kernels  3 fusion kernels  4 shm kernels
+ *   5 kernel cost total  6 remaps  7 plan time (us)  8 staging exact (1/0)
+ *   9 L  10 G  11 device launches per run */
+atlas_status atlas_plan_stats(atlas_ctx *ctx, int64_t *out, int cap);
+
+/* Per-launch records of the last atlas_run (needs option "timing" = 1):
+ * ms[i] device time, kind[i] (0 init, 1 fused, 2 shm, 3 pack, 4 exchange,
+ * 5 scale), bytes[i] algorithmic HBM bytes of that launch (read + write of
+ * the amplitudes it touches).  *count receives the number of records. */
+atlas_status atlas_get_launches(atlas_ctx *ctx, float *ms, int32_t *kind,
+                                int64_t *bytes, int cap, int *count);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* ATLAS_H_ */

@@ -1,0 +1,270 @@
+// capi.cpp -- extern "C" entry points declared in include/atlas.h.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "ctx.h"
+
+namespace atlas {
+const char *last_error_cstr();
+void build_plan(atlas_ctx *C, int s_max, double cf);
+std::string plan_json(const atlas_ctx *C);
+void run(atlas_ctx *C);
+void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count);
+void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count);
+void destroy(atlas_ctx *C);
+void nccl_unique_id(void *out);
+}  // namespace atlas
+
+using namespace atlas;
+
+#define GUARD(body)                           \
+  try {                                       \
+    set_last_error("");                       \
+    body;                                     \
+    return ATLAS_OK;                          \
+  } catch (const Error &e) {                  \
+    set_last_error(e.msg);                    \
+    return e.st;                              \
+  } catch (const std::bad_alloc &) {          \
+    set_last_error("host allocation failed"); \
+    return ATLAS_E_OOM;                       \
+  } catch (...) {                             \
+    set_last_error("unknown internal error"); \
+    return ATLAS_E_INVALID;                   \
+  }
+
+static void need(bool c, atlas_status st, const char *msg) {
+  if (!c) fail(st, "%s", msg);
+}
+
+extern "C" {
+
+const char *atlas_last_error(void) { return last_error_cstr(); }
+
+atlas_status atlas_create(int n, atlas_dtype dtype, int world, int rank, const void *nccl_uid,
+                          atlas_ctx **out) {
+  GUARD({
+    need(out != nullptr, ATLAS_E_INVALID, "out is NULL");
+    *out = nullptr;
+    need(n >= 1 && n <= 48, ATLAS_E_INVALID, "n must be in [1, 48]");
+    need(world >= 1 && world <= 64 && (world & (world - 1)) == 0, ATLAS_E_INVALID,
+         "world must be a power of two in [1, 64]");
+    need(rank >= 0 && rank < world, ATLAS_E_INVALID, "rank out of range");
+    need(dtype == ATLAS_C128 || dtype == ATLAS_C64, ATLAS_E_UNSUPPORTED, "unknown dtype");
+    int G = __builtin_ctz((unsigned)world);
+    need(G < n, ATLAS_E_INVALID, "log2(world) must be < n");
+    atlas_ctx *C = new atlas_ctx();
+    C->n = n;
+    C->world = world;
+    C->rank = rank;
+    C->G = G;
+    C->L = n - G;
+    C->dt = dtype;
+    C->opt.ls_qubits = -1;
+    if (nccl_uid) {
+      memcpy(C->nccl_uid, nccl_uid, 128);
+      C->have_uid = true;
+    }
+    *out = C;
+  })
+}
+
+atlas_status atlas_load_circuit(atlas_ctx *C, const atlas_gate *gates, size_t m) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    need(m == 0 || gates != nullptr, ATLAS_E_INVALID, "gates is NULL");
+    std::vector<Gate> v;
+    v.reserve(m);
+    for (size_t i = 0; i < m; i++) {
+      const atlas_gate &a = gates[i];
+      int ar = kind_arity((int)a.kind);
+      if (ar < 0) fail(ATLAS_E_UNSUPPORTED, "gate %zu: unknown kind %u", i, a.kind);
+      if ((int)a.nq != ar) fail(ATLAS_E_INVALID, "gate %zu: %s takes %d qubits, got %u", i, kind_name(a.kind), ar, a.nq);
+      Gate g;
+      g.kind = (int)a.kind;
+      g.nq = ar;
+      for (int j = 0; j < 3; j++) g.q[j] = j < ar ? (int)a.q[j] : 0;
+      for (int j = 0; j < ar; j++) {
+        if (a.q[j] >= (uint32_t)C->n) fail(ATLAS_E_INVALID, "gate %zu: qubit %u out of range", i, a.q[j]);
+        for (int l = 0; l < j; l++)
+          if (a.q[l] == a.q[j]) fail(ATLAS_E_INVALID, "gate %zu: duplicate operand %u", i, a.q[j]);
+      }
+      for (int j = 0; j < 4; j++) {
+        g.p[j] = a.p[j];
+        if (!std::isfinite(g.p[j])) fail(ATLAS_E_INVALID, "gate %zu: non-finite parameter", i);
+      }
+      v.push_back(g);
+    }
+    C->gates.swap(v);
+    C->planned = false;
+  })
+}
+
+atlas_status atlas_plan(atlas_ctx *C, int s_max, double c) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    need(s_max >= 1, ATLAS_E_INVALID, "s_max must be >= 1");
+    need(c >= 0 && std::isfinite(c), ATLAS_E_INVALID, "c must be finite and >= 0");
+    build_plan(C, s_max, c);
+  })
+}
+
+atlas_status atlas_run(atlas_ctx *C) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    run(C);
+  })
+}
+
+atlas_status atlas_get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
+  GUARD({
+    need(C != nullptr && (host != nullptr || count == 0), ATLAS_E_INVALID, "NULL argument");
+    get_state(C, host, first, count);
+  })
+}
+
+atlas_status atlas_set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
+  GUARD({
+    need(C != nullptr && (host != nullptr || count == 0), ATLAS_E_INVALID, "NULL argument");
+    set_state(C, host, first, count);
+  })
+}
+
+void atlas_destroy(atlas_ctx *C) {
+  if (!C) return;
+  try {
+    destroy(C);
+  } catch (...) {
+  }
+}
+
+atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
+  GUARD({
+    need(C != nullptr && key != nullptr, ATLAS_E_INVALID, "NULL argument");
+    std::string k(key);
+    Options &o = C->opt;
+    bool replan = true;
+    if (k == "kernelizer") { need(v >= 0 && v <= 2, ATLAS_E_INVALID, "kernelizer in 0..2"); o.kernelizer = (int)v; }
+    else if (k == "prune_T") o.prune_T = (int)v;
+    else if (k == "ls_qubits") { need(v >= 0 && v <= 13, ATLAS_E_INVALID, "ls_qubits in 0..13"); o.ls_qubits = (int)v; }
+    else if (k == "shm_qubits") o.shm_qubits = (int)v;
+    else if (k == "fusion_qubits") o.fusion_qubits = (int)v;
+    else if (k == "kinds") { need(v >= 1 && v <= 3, ATLAS_E_INVALID, "kinds in 1..3"); o.kinds = (int)v; }
+    else if (k == "insular_lift") o.lift = (int)v;
+    else if (k == "attach") o.attach = (int)v;
+    else if (k == "virtual_world") {
+      need(!C->dev_ready, ATLAS_E_ORDER, "virtual_world must be set before the first run");
+      o.virtual_world = (int)v;
+    } else if (k == "init") { o.init = (int)v; replan = false; }
+    else if (k == "timing") { o.timing = (int)v; replan = false; }
+    else if (k == "device") { need(!C->dev_ready, ATLAS_E_ORDER, "device must be set before the first run"); o.device = (int)v; replan = false; }
+    else if (k == "stage_budget") o.stage_budget = (long)v;
+    else fail(ATLAS_E_UNSUPPORTED, "unknown option '%s'", key);
+    if (replan) C->planned = false;
+  })
+}
+
+atlas_status atlas_set_option_str(atlas_ctx *C, const char *key, const char *value) {
+  GUARD({
+    need(C != nullptr && key != nullptr, ATLAS_E_INVALID, "NULL argument");
+    std::string k(key);
+    if (k == "cost_model") C->opt.cost_model = value ? value : "";
+    else fail(ATLAS_E_UNSUPPORTED, "unknown option '%s'", key);
+    C->planned = false;
+  })
+}
+
+atlas_status atlas_bind_buffers(atlas_ctx *C, void *state, void *scratch, uint64_t bytes) {
+  GUARD({
+    need(C != nullptr && state != nullptr, ATLAS_E_INVALID, "NULL argument");
+    need(!C->dev_ready, ATLAS_E_ORDER, "bind buffers before the first run");
+    need(C->world == 1 || C->opt.virtual_world == 0, ATLAS_E_UNSUPPORTED,
+         "bind_buffers is not supported in virtual-world mode");
+    size_t need_b = (C->dt == ATLAS_C128 ? 16ull : 8ull) << C->L;
+    need(bytes >= need_b, ATLAS_E_INVALID, "buffers too small for 2^L amplitudes");
+    need(C->world == 1 || scratch != nullptr, ATLAS_E_INVALID, "world > 1 needs a scratch buffer");
+    C->nslots = 1;
+    C->d_state.assign(1, state);
+    C->d_scratch.assign(1, scratch);
+    C->bound = true;
+  })
+}
+
+atlas_status atlas_set_stream(atlas_ctx *C, void *stream) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    if (C->own_stream && C->stream) {
+      cudaStreamSynchronize(C->stream);
+      cudaStreamDestroy(C->stream);
+    }
+    C->stream = (cudaStream_t)stream;
+    C->own_stream = false;
+  })
+}
+
+atlas_status atlas_nccl_unique_id(void *out128) {
+  GUARD({
+    need(out128 != nullptr, ATLAS_E_INVALID, "NULL argument");
+    nccl_unique_id(out128);
+  })
+}
+
+atlas_status atlas_get_plan_json(atlas_ctx *C, char *buf, size_t cap, size_t *len) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    need(C->planned, ATLAS_E_ORDER, "no plan");
+    std::string s = plan_json(C);
+    if (len) *len = s.size();
+    if (buf && cap) {
+      size_t k = std::min(cap - 1, s.size());
+      memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+  })
+}
+
+atlas_status atlas_plan_stats(atlas_ctx *C, int64_t *out, int cap) {
+  GUARD({
+    need(C != nullptr && out != nullptr, ATLAS_E_INVALID, "NULL argument");
+    need(C->planned, ATLAS_E_ORDER, "no plan");
+    int64_t v[12] = {0};
+    v[0] = C->sp.s;
+    v[1] = (int64_t)llround(C->sp.cost * 1000);
+    for (auto &kp : C->kplans) {
+      for (auto &K : kp.kernels) {
+        v[2]++;
+        if (K.kind == K_FUSION) v[3]++;
+        else v[4]++;
+      }
+      v[5] += kp.total;
+    }
+    for (int k = 1; k < C->sp.s; k++)
+      if (C->exch[k].gp > 0) v[6]++;
+    v[7] = (int64_t)C->plan_us;
+    v[8] = C->sp.exact ? 1 : 0;
+    v[9] = C->L;
+    v[10] = C->G;
+    int64_t nl = 0;
+    for (auto &ln : C->prog[0])
+      if (ln.type == L_FUSED || ln.type == L_SHM || ln.type == L_SCALE || ln.type == L_PACK) nl++;
+    v[11] = nl;
+    for (int i = 0; i < cap && i < 12; i++) out[i] = v[i];
+  })
+}
+
+atlas_status atlas_get_launches(atlas_ctx *C, float *ms, int32_t *kind, int64_t *bytes, int cap,
+                                int *count) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    int n = (int)C->launch_ms.size();
+    if (count) *count = n;
+    for (int i = 0; i < n && i < cap; i++) {
+      if (ms) ms[i] = C->launch_ms[i];
+      if (kind) kind[i] = C->launch_kind[i];
+      if (bytes) bytes[i] = C->launch_bytes[i];
+    }
+  })
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// ctx.h -- the atlas_ctx object: circuit, plan, lowered device programs.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "device.h"
+#include "internal.h"
+
+namespace atlas {
+
+enum LaunchType { L_INIT = 0, L_FUSED = 1, L_SHM = 2, L_PACK = 3, L_EXCHANGE = 4, L_SCALE = 5 };
+
+struct Launch {
+  int type = 0;
+  int stage = 0;
+  FusedLaunch fl{};
+  ShmLaunch sl{};
+  int64_t newpos_off = -1;   // L_PACK: offset into newpos blob (L ints)
+  double sre = 1, sim = 0;   // L_SCALE
+  int64_t bytes = 0;         // algorithmic HBM bytes
+};
+
+// Exchange of one remap (stage boundary k-1 -> k): swap the g' top local
+// slots with the incoming qubits' global slots.
+struct Exchange {
+  int gp = 0;                   // g'
+  std::vector<int> gamma;       // global slot offsets (slot - L) of incoming qubits, j-th
+  std::vector<int> fI;          // flip of the j-th incoming qubit before the exchange
+  bool packed = false;          // a pack launch precedes (source = scratch)
+};
+
+struct StageMap {
+  std::vector<int> sigma;       // logical -> physical slot during the stage
+  std::vector<int> flip_end;    // per logical qubit: flip bit at the end of the stage
+  std::vector<int> flip_begin;  // at the start
+};
+
+struct Options {
+  int kernelizer = 0;
+  int prune_T = 500;
+  int ls_qubits = 5;
+  int shm_qubits = -1;
+  int fusion_qubits = -1;
+  int kinds = 3;
+  int lift = 1;
+  int attach = 1;
+  int virtual_world = 0;
+  int init = 1;
+  int timing = 0;
+  int device = -1;
+  long stage_budget = 2000000;
+  std::string cost_model;
+};
+
+struct NcclApi;
+
+}  // namespace atlas
+
+struct atlas_ctx {
+  int n = 0, world = 1, rank = 0, G = 0, L = 0;
+  atlas_dtype dt = ATLAS_C128;
+  atlas::Options opt;
+  unsigned char nccl_uid[128];
+  bool have_uid = false;
+
+  std::vector<atlas::Gate> gates;
+  std::vector<atlas::GateInfo> info;
+
+  // plan
+  bool planned = false;
+  double plan_us = 0;
+  double c = 3;
+  atlas::CostModel cm;
+  atlas::StagePlan sp;
+  std::vector<atlas::StageMap> maps;
+  std::vector<std::vector<int>> stage_gates;     // circuit ids per stage (order)
+  std::vector<atlas::KernelPlan> kplans;         // per stage; gate ids = circuit ids
+  std::vector<atlas::Exchange> exch;             // per stage (index 0 unused)
+  int K_tile = 0;
+
+  // lowered programs: one per simulated rank (world in virtual mode, else 1)
+  int nslots = 1;
+  std::vector<std::vector<atlas::Launch>> prog;
+  std::vector<uint64_t> hightab;
+  std::vector<atlas::ShmOp> ops;
+  std::vector<atlas::ShmPhase> phases;
+  std::vector<double2> mats;
+  std::vector<int> newpos;
+
+  // device
+  bool dev_ready = false, blobs_ready = false;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<void *> d_state, d_scratch;  // per slot
+  std::vector<int> cur;                    // 0: state holds the data, 1: scratch
+  bool bound = false;
+  void *d_hightab = nullptr, *d_ops = nullptr, *d_phases = nullptr, *d_mats = nullptr,
+       *d_newpos = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<float> launch_ms;
+  std::vector<int> launch_kind;
+  std::vector<int64_t> launch_bytes;
+  void *nccl_comm = nullptr;
+  bool state_set = false;
+};

@@ -1,0 +1,643 @@
+// plan.cpp -- Partition (Alg. 1) and lowering.
+//
+//   classify  -> stage (staging.cpp) -> placement + remap schedule
+//   -> per stage: insular specialisation per rank -> Kernelize -> lowering to
+//      device launches (fused matrices / shared-memory op programs).
+//
+// Placement (R6): stage 0 puts the local qubits that leave at the
+// first remap in the top local slots; every remap swaps the top g' local slots
+// with the incoming qubits' global slots (one all-to-all of contiguous blocks),
+// preceded by a local bit-permutation ("pack") only when the outgoing qubits
+// are not already in the top slots.
+//
+// Insular specialisation: a gate's global operands are insular
+// (staging guarantees it) and their values are known per rank, so the gate
+// restricted to those values is a smaller gate on its local operands, the
+// identity, or a scalar.  An anti-diagonal gate on a global qubit is a
+// relabelling: it toggles the qubit's flip bit (R14); the factor of
+// Y-like gates becomes a per-rank scalar (R15).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "ctx.h"
+
+namespace atlas {
+
+extern const char *kBuiltinModelC128;
+extern const char *kBuiltinModelC64;
+int shm_register_bits(int K);
+
+CostModel builtin_cost_model(atlas_dtype dt) {
+  return load_cost_model(dt == ATLAS_C128 ? kBuiltinModelC128 : kBuiltinModelC64, true);
+}
+
+namespace {
+
+struct LGate {
+  int nl = 0;
+  int lq[3];        // local operands (logical), operand order
+  Role lrole[3];
+  cd M[64];         // 2^nl x 2^nl
+  bool identity = false;
+};
+
+bool is_identity(const cd *M, int d) {
+  for (int r = 0; r < d; r++)
+    for (int c = 0; c < d; c++)
+      if (std::abs(M[r * d + c] - (r == c ? cd(1) : cd(0))) > 1e-15) return false;
+  return true;
+}
+
+// value of logical qubit q on rank `rank` during a stage (q global)
+int global_value(const StageMap &mp, int L, int rank, int q, const std::vector<int> &flip) {
+  int slot = mp.sigma[q];
+  return ((rank >> (slot - L)) & 1) ^ flip[q];
+}
+
+u64 ls_logical(const std::vector<int> &sigma, int ls) {
+  u64 s = 0;
+  for (int q = 0; q < (int)sigma.size(); q++)
+    if (sigma[q] < ls) s |= 1ull << q;
+  return s;
+}
+
+}  // namespace
+
+void build_plan(atlas_ctx *C, int s_max, double cf) {
+  auto t0 = std::chrono::steady_clock::now();
+  const int n = C->n, L = C->L, G = C->G, m = (int)C->gates.size();
+  // ---- cost model
+  C->cm = C->opt.cost_model.empty() ? builtin_cost_model(C->dt)
+                                    : load_cost_model(C->opt.cost_model, false);
+  if (C->opt.shm_qubits >= 0) C->cm.q_max_shared = C->opt.shm_qubits;
+  if (C->opt.fusion_qubits >= 0) C->cm.q_max_fusion = C->opt.fusion_qubits;
+  if (C->opt.ls_qubits >= 0) C->cm.ls_qubits = C->opt.ls_qubits;
+  C->cm.q_max_fusion = std::min(C->cm.q_max_fusion, 5);   // fused templates k <= 5
+  C->cm.q_max_shared = std::min(C->cm.q_max_shared, 13);  // shm templates K <= 13
+  if ((int)C->cm.fusion_cost.size() < C->cm.q_max_fusion)
+    fail(ATLAS_E_INVALID, "cost model fusion table too short");
+  // ---- a1: insular classification
+  C->info.resize(m);
+  for (int g = 0; g < m; g++) C->info[g] = classify(C->gates[g]);
+  // ---- a2: staging
+  C->c = cf;
+  C->sp = stage_circuit(n, L, G, C->info, s_max, cf, C->opt.stage_budget);
+  const int s = C->sp.s;
+  C->stage_gates.assign(s, {});
+  for (int g = 0; g < m; g++) C->stage_gates[C->sp.gate_stage[g]].push_back(g);
+  // ---- placement and remap schedule
+  C->maps.assign(s, {});
+  C->exch.assign(s, {});
+  {
+    std::vector<int> sigma(n, -1), flip(n, 0);
+    u64 loc0 = C->sp.local[0];
+    u64 out1 = s > 1 ? (loc0 & ~C->sp.local[1]) : 0;
+    int slot = 0;
+    for (int q = 0; q < n; q++)
+      if (((loc0 >> q) & 1) && !((out1 >> q) & 1)) sigma[q] = slot++;
+    for (int q = 0; q < n; q++)
+      if ((out1 >> q) & 1) sigma[q] = slot++;
+    for (int q = 0; q < n; q++)
+      if (!((loc0 >> q) & 1)) sigma[q] = slot++;
+    C->maps[0].sigma = sigma;
+    C->maps[0].flip_begin = flip;
+  }
+  // flips evolve inside a stage (anti-diagonal gates on global qubits); the
+  // end-of-stage flips are filled by the specialisation pass below, and the
+  // next stage's mapping is derived from them, so do both per stage.
+  C->K_tile = 0;
+  {
+    int qms = std::min(C->cm.q_max_shared, L);
+    C->K_tile = (qms >= 6 && (C->opt.kinds & 2)) ? qms : 0;
+  }
+  C->nslots = (C->opt.virtual_world && C->world > 1) ? C->world : 1;
+  C->prog.assign(C->nslots, {});
+  C->hightab.clear();
+  C->ops.clear();
+  C->phases.clear();
+  C->mats.clear();
+  C->newpos.clear();
+  C->kplans.assign(s, {});
+  const int B = C->dt == ATLAS_C128 ? 16 : 8;
+  const int64_t pass_bytes = 2 * ((int64_t)B << L);
+  auto slot_rank = [&](int sl) { return C->nslots > 1 ? sl : C->rank; };
+
+  for (int k = 0; k < s; k++) {
+    StageMap &mp = C->maps[k];
+    // ---- remap from stage k-1
+    if (k > 0) {
+      const StageMap &pm = C->maps[k - 1];
+      std::vector<int> sigma = pm.sigma, flip = pm.flip_end;
+      u64 O = C->sp.local[k - 1] & ~C->sp.local[k];
+      u64 I = C->sp.local[k] & ~C->sp.local[k - 1];
+      int gp = popc(O);
+      Exchange &ex = C->exch[k];
+      ex.gp = gp;
+      // pack if the outgoing qubits are not exactly the top gp local slots
+      std::vector<int> at(n, -1);
+      for (int q = 0; q < n; q++) at[sigma[q]] = q;
+      bool ok = true;
+      for (int j = 0; j < gp; j++)
+        if (!((O >> at[L - gp + j]) & 1)) ok = false;
+      if (!ok && gp > 0) {
+        std::vector<int> newslot(n);
+        for (int i = 0; i < n; i++) newslot[i] = i;
+        std::vector<int> vac, disp;
+        std::vector<int> outs;
+        for (int q = 0; q < n; q++)
+          if ((O >> q) & 1) outs.push_back(q);
+        for (int q : outs)
+          if (sigma[q] < L - gp) vac.push_back(sigma[q]);
+        for (int sl = L - gp; sl < L; sl++)
+          if (!((O >> at[sl]) & 1)) disp.push_back(sl);
+        std::sort(vac.begin(), vac.end());
+        std::sort(disp.begin(), disp.end());
+        for (size_t i = 0; i < disp.size(); i++) newslot[disp[i]] = vac[i];
+        // outgoing qubits fill the top slots in ascending logical order
+        int j = 0;
+        for (int q : outs) newslot[sigma[q]] = L - gp + (j++);
+        // check it is a permutation of the local slots
+        std::vector<int> seen(L, 0);
+        for (int i = 0; i < L; i++) seen[newslot[i]]++;
+        for (int i = 0; i < L; i++)
+          if (seen[i] != 1) fail(ATLAS_E_INVALID, "internal: pack is not a permutation");
+        int64_t off = (int64_t)C->newpos.size();
+        for (int i = 0; i < L; i++) C->newpos.push_back(newslot[i]);
+        for (int q = 0; q < n; q++) sigma[q] = newslot[sigma[q]];
+        for (int sl = 0; sl < C->nslots; sl++) {
+          Launch ln;
+          ln.type = L_PACK;
+          ln.stage = k;
+          ln.newpos_off = off;
+          ln.bytes = pass_bytes;
+          C->prog[sl].push_back(ln);
+        }
+        ex.packed = true;
+        for (int q = 0; q < n; q++) at[sigma[q]] = q;
+      }
+      std::vector<int> ins;
+      for (int q = 0; q < n; q++)
+        if ((I >> q) & 1) ins.push_back(q);
+      ex.gamma.clear();
+      ex.fI.clear();
+      for (int j = 0; j < gp; j++) {
+        int oq = at[L - gp + j], iq = ins[j];
+        int gslot = sigma[iq];
+        ex.gamma.push_back(gslot - L);
+        ex.fI.push_back(flip[iq]);
+        sigma[iq] = L - gp + j;
+        sigma[oq] = gslot;
+        flip[iq] = 0;
+        flip[oq] = 0;
+      }
+      if (gp > 0)
+        for (int sl = 0; sl < C->nslots; sl++) {
+          Launch ln;
+          ln.type = L_EXCHANGE;
+          ln.stage = k;
+          ln.bytes = (int64_t)(((double)(B) * (double)(1ull << L)) * (1.0 - std::ldexp(1.0, -gp)));
+          C->prog[sl].push_back(ln);
+        }
+      mp.sigma = sigma;
+      mp.flip_begin = flip;
+    }
+    // ---- insular specialisation, in circuit order, per simulated rank
+    const std::vector<int> &ids = C->stage_gates[k];
+    std::vector<int> flip = mp.flip_begin;
+    std::vector<std::vector<LGate>> lg(C->nslots, std::vector<LGate>(ids.size()));
+    std::vector<cd> scalar(C->nslots, cd(1));
+    std::vector<KGate> seq;
+    std::vector<int> seq_pos;  // position in ids
+    for (size_t ii = 0; ii < ids.size(); ii++) {
+      const Gate &g = C->gates[ids[ii]];
+      const GateInfo &gi = C->info[ids[ii]];
+      const int ka = kind_arity(g.kind);
+      cd M[64];
+      gate_matrix(g, M);
+      const int d = 1 << ka;
+      int nl = 0;
+      for (int j = 0; j < ka; j++)
+        if (mp.sigma[g.q[j]] < L) nl++;
+      if (nl == 0) {
+        // every operand global and insular
+        if (ka == 1 && gi.role[0] == ANTI) {
+          int q = g.q[0];
+          for (int sl = 0; sl < C->nslots; sl++) {
+            int v_new = global_value(mp, L, slot_rank(sl), q, flip) ^ 1;
+            scalar[sl] *= M[v_new * 2 + (1 - v_new)];
+          }
+          flip[q] ^= 1;
+        } else {
+          for (int sl = 0; sl < C->nslots; sl++) {
+            int sel = 0;
+            for (int j = 0; j < ka; j++)
+              sel |= global_value(mp, L, slot_rank(sl), g.q[j], flip) << j;
+            scalar[sl] *= M[sel * d + sel];
+          }
+        }
+        continue;
+      }
+      KGate kg;
+      kg.gid = ids[ii];
+      kg.qubits = kg.active = kg.diagq = kg.antiq = 0;
+      kg.kind = g.kind;
+      for (int j = 0; j < ka; j++) {
+        int q = g.q[j];
+        if (mp.sigma[q] >= L) {
+          if (gi.role[j] == TGT || gi.role[j] == ANTI)
+            fail(ATLAS_E_INVALID, "internal: non-insular operand of gate %d is global", ids[ii]);
+          continue;
+        }
+        kg.qubits |= 1ull << q;
+        if (gi.role[j] == TGT || gi.role[j] == ANTI) kg.active |= 1ull << q;
+        if (gi.role[j] == ANTI) kg.antiq |= 1ull << q;
+        if (gi.role[j] == CTL || gi.role[j] == DIAG) kg.diagq |= 1ull << q;
+      }
+      seq.push_back(kg);
+      seq_pos.push_back((int)ii);
+      for (int sl = 0; sl < C->nslots; sl++) {
+        LGate &x = lg[sl][ii];
+        x.nl = 0;
+        int kv[3], lpos[3];
+        for (int j = 0; j < ka; j++) {
+          int q = g.q[j];
+          if (mp.sigma[q] >= L) {
+            kv[j] = global_value(mp, L, slot_rank(sl), q, flip);
+            lpos[j] = -1;
+          } else {
+            kv[j] = -1;
+            lpos[j] = x.nl;
+            x.lq[x.nl] = q;
+            x.lrole[x.nl] = gi.role[j];
+            x.nl++;
+          }
+        }
+        const int dl = 1 << x.nl;
+        for (int r = 0; r < dl; r++)
+          for (int c = 0; c < dl; c++) {
+            int R = 0, Cc = 0;
+            for (int j = 0; j < ka; j++) {
+              int br = kv[j] >= 0 ? kv[j] : ((r >> lpos[j]) & 1);
+              int bc = kv[j] >= 0 ? kv[j] : ((c >> lpos[j]) & 1);
+              R |= br << j;
+              Cc |= bc << j;
+            }
+            x.M[r * dl + c] = M[R * d + Cc];
+          }
+        x.identity = is_identity(x.M, dl);
+      }
+    }
+    mp.flip_end = flip;
+    // ---- a3: kernelization of the stage
+    KernelizeOptions ko;
+    ko.algo = C->opt.kernelizer;
+    ko.prune_T = C->opt.prune_T;
+    ko.lift = C->opt.lift != 0;
+    ko.attach = C->opt.attach != 0;
+    ko.kinds = C->opt.kinds;
+    ko.L = L;
+    ko.ls_set = ls_logical(mp.sigma, std::min(C->cm.ls_qubits, L));
+    KernelPlan kp;
+    if (!seq.empty()) {
+      if (ko.algo == 1) kp = ordered_kernelize(seq, C->cm, ko);
+      else if (ko.algo == 2) kp = greedy_kernelize(seq, C->cm, ko);
+      else kp = dp_kernelize(seq, C->cm, ko);
+    }
+    // kernel gate indices are positions in seq; keep them for lowering and
+    // translate to circuit ids for the plan report
+    C->kplans[k] = kp;
+    for (auto &K : C->kplans[k].kernels)
+      for (auto &gidx : K.gates) gidx = seq[gidx].gid;
+    // ---- a4: lowering per simulated rank
+    for (int sl = 0; sl < C->nslots; sl++) {
+      bool scalar_done = std::abs(scalar[sl] - cd(1)) < 1e-15;
+      for (const Kernel &K : kp.kernels) {
+        // skip kernels that are the identity on this rank
+        bool all_id = true;
+        for (int gi : K.gates)
+          if (!lg[sl][seq_pos[gi]].identity) all_id = false;
+        if (all_id && scalar_done) continue;
+        Launch ln;
+        ln.stage = k;
+        ln.bytes = pass_bytes;
+        if (K.kind == K_FUSION) {
+          ln.type = L_FUSED;
+          std::vector<int> slots;
+          u64 qs = K.qubits;
+          while (qs) {
+            int q = ctz(qs);
+            qs &= qs - 1;
+            slots.push_back(mp.sigma[q]);
+          }
+          std::sort(slots.begin(), slots.end());
+          const int kk = (int)slots.size();
+          const int D = 1 << kk;
+          ln.fl.k = kk;
+          for (int j = 0; j < 6; j++) ln.fl.t[j] = j < kk ? slots[j] : 0;
+          // matrix = product of the member gates in kernel order
+          std::vector<cd> U(D * D, cd(0));
+          for (int i = 0; i < D; i++) U[i * D + i] = 1;
+          for (int gi : K.gates) {
+            const LGate &x = lg[sl][seq_pos[gi]];
+            if (x.identity) continue;
+            int bitpos[3];
+            for (int j = 0; j < x.nl; j++)
+              bitpos[j] = (int)(std::find(slots.begin(), slots.end(), mp.sigma[x.lq[j]]) - slots.begin());
+            const int dl = 1 << x.nl;
+            int mask = 0;
+            for (int j = 0; j < x.nl; j++) mask |= 1 << bitpos[j];
+            for (int col = 0; col < D; col++) {
+              for (int b = 0; b < D; b++) {
+                if (b & mask) continue;
+                cd v[8], w[8];
+                for (int c = 0; c < dl; c++) {
+                  int idx = b;
+                  for (int j = 0; j < x.nl; j++)
+                    if ((c >> j) & 1) idx |= 1 << bitpos[j];
+                  v[c] = U[idx * D + col];
+                }
+                for (int r = 0; r < dl; r++) {
+                  w[r] = 0;
+                  for (int c = 0; c < dl; c++) w[r] += x.M[r * dl + c] * v[c];
+                }
+                for (int r = 0; r < dl; r++) {
+                  int idx = b;
+                  for (int j = 0; j < x.nl; j++)
+                    if ((r >> j) & 1) idx |= 1 << bitpos[j];
+                  U[idx * D + col] = w[r];
+                }
+              }
+            }
+          }
+          if (!scalar_done) {
+            for (auto &z : U) z *= scalar[sl];
+            scalar_done = true;
+          }
+          ln.fl.mat_off = (int64_t)C->mats.size();
+          for (auto &z : U) C->mats.push_back(make_double2(z.real(), z.imag()));
+        } else {
+          ln.type = L_SHM;
+          const int K_ = C->K_tile;
+          const int RB = shm_register_bits(K_);
+          // active slots: kernel qubits (active set + LSB) padded to K_ slots
+          u64 amask = 0;
+          u64 qs = K.qubits;
+          while (qs) {
+            int q = ctz(qs);
+            qs &= qs - 1;
+            amask |= 1ull << mp.sigma[q];
+          }
+          for (int sl2 = 0; sl2 < L && popc(amask) < K_; sl2++) amask |= 1ull << sl2;
+          if (popc(amask) != K_) fail(ATLAS_E_INVALID, "internal: shm active set %d != K %d", popc(amask), K_);
+          std::vector<int> act;
+          for (int b = 0; b < L; b++)
+            if ((amask >> b) & 1) act.push_back(b);
+          int c0 = 0;
+          while (c0 < K_ && act[c0] == c0) c0++;
+          std::vector<int> tile_of_slot(L, -1);
+          for (int b = 0; b < K_; b++) tile_of_slot[act[b]] = b;
+          ln.sl.K = K_;
+          ln.sl.RB = RB;
+          ln.sl.c0 = c0;
+          const u64 lmask = (L == 64) ? ~0ull : ((1ull << L) - 1);
+          ln.sl.nonactive = lmask & ~amask;
+          ln.sl.ntiles = 1ull << (L - K_);
+          ln.sl.hightab_off = (int64_t)C->hightab.size();
+          for (u64 h = 0; h < (1ull << (K_ - c0)); h++) {
+            u64 off = 0;
+            for (int b = c0; b < K_; b++)
+              if ((h >> (b - c0)) & 1) off |= 1ull << act[b];
+            C->hightab.push_back(off);
+          }
+          // ops (tile-bit targets first; register indices resolved per phase)
+          struct Pre {
+            ShmOp op;
+            int ttile[2];
+            int nt;
+            int sel_slot[3];
+          };
+          std::vector<Pre> pre;
+          if (!scalar_done) {
+            Pre p{};
+            p.op.type = OP_DIAG;
+            p.op.nsel = 0;
+            p.op.m[0] = scalar[sl].real();
+            p.op.m[1] = scalar[sl].imag();
+            p.nt = 0;
+            pre.push_back(p);
+            scalar_done = true;
+          }
+          for (int gi : K.gates) {
+            const LGate &x = lg[sl][seq_pos[gi]];
+            if (x.identity) continue;
+            int tj[3], sj[3], nt = 0, ns = 0;
+            for (int j = 0; j < x.nl; j++) {
+              if (x.lrole[j] == TGT || x.lrole[j] == ANTI) tj[nt++] = j;
+              else sj[ns++] = j;
+            }
+            const int dl = 1 << x.nl;
+            const int dt = 1 << nt;
+            for (int sv = 0; sv < (1 << ns); sv++) {
+              // block for selector value sv
+              cd blk[16];
+              bool ident = true;
+              bool offsel = false;  // entries mixing selector values must vanish
+              for (int r = 0; r < dt; r++)
+                for (int c = 0; c < dt; c++) {
+                  int R = 0, Cc = 0;
+                  for (int a = 0; a < nt; a++) {
+                    R |= ((r >> a) & 1) << tj[a];
+                    Cc |= ((c >> a) & 1) << tj[a];
+                  }
+                  for (int a = 0; a < ns; a++) {
+                    R |= ((sv >> a) & 1) << sj[a];
+                    Cc |= ((sv >> a) & 1) << sj[a];
+                  }
+                  blk[r * dt + c] = x.M[R * dl + Cc];
+                  if (std::abs(blk[r * dt + c] - (r == c ? cd(1) : cd(0))) > 1e-15) ident = false;
+                }
+              (void)offsel;
+              if (nt == 0) {
+                // diagonal: collect all selector values into one DIAG op
+                if (sv == 0) {
+                  Pre p{};
+                  p.op.type = OP_DIAG;
+                  p.op.nsel = ns;
+                  p.nt = 0;
+                  for (int a = 0; a < ns; a++) p.sel_slot[a] = mp.sigma[x.lq[sj[a]]];
+                  pre.push_back(p);
+                }
+                pre.back().op.m[2 * sv] = blk[0].real();
+                pre.back().op.m[2 * sv + 1] = blk[0].imag();
+                continue;
+              }
+              if (ident) continue;
+              Pre p{};
+              p.nt = nt;
+              p.op.nsel = ns;
+              p.op.selv = sv;
+              for (int a = 0; a < ns; a++) p.sel_slot[a] = mp.sigma[x.lq[sj[a]]];
+              for (int a = 0; a < nt; a++) {
+                int ts = tile_of_slot[mp.sigma[x.lq[tj[a]]]];
+                if (ts < 0) fail(ATLAS_E_INVALID, "internal: shm target not active");
+                p.ttile[a] = ts;
+              }
+              if (nt == 1) {
+                bool isx = std::abs(blk[0]) < 1e-15 && std::abs(blk[3]) < 1e-15 &&
+                           std::abs(blk[1] - cd(1)) < 1e-15 && std::abs(blk[2] - cd(1)) < 1e-15;
+                p.op.type = isx ? OP_PERM1 : OP_DENSE1;
+                for (int i = 0; i < 4; i++) {
+                  p.op.m[2 * i] = blk[i].real();
+                  p.op.m[2 * i + 1] = blk[i].imag();
+                }
+              } else if (nt == 2) {
+                p.op.type = OP_DENSE2;
+                // canonical order: ttile[0] < ttile[1]
+                if (p.ttile[0] > p.ttile[1]) {
+                  std::swap(p.ttile[0], p.ttile[1]);
+                  cd b2[16];
+                  for (int r = 0; r < 4; r++)
+                    for (int c = 0; c < 4; c++) {
+                      int rs = ((r & 1) << 1) | (r >> 1), cs = ((c & 1) << 1) | (c >> 1);
+                      b2[rs * 4 + cs] = blk[r * 4 + c];
+                    }
+                  std::copy(b2, b2 + 16, blk);
+                }
+                for (int i = 0; i < 16; i++) {
+                  p.op.m[2 * i] = blk[i].real();
+                  p.op.m[2 * i + 1] = blk[i].imag();
+                }
+              } else {
+                fail(ATLAS_E_UNSUPPORTED, "internal: gate with %d targets in shm kernel", nt);
+              }
+              pre.push_back(p);
+            }
+          }
+          // register phases: greedy grouping by target tile bits (<= RB)
+          std::vector<std::pair<int, std::vector<int>>> groups;  // (mask, op indices)
+          for (int i = 0; i < (int)pre.size(); i++) {
+            int tm = 0;
+            for (int a = 0; a < pre[i].nt; a++) tm |= 1 << pre[i].ttile[a];
+            if (groups.empty() || popc((u64)(groups.back().first | tm)) > RB)
+              groups.push_back({tm, {i}});
+            else {
+              groups.back().first |= tm;
+              groups.back().second.push_back(i);
+            }
+          }
+          if (groups.empty()) groups.push_back({0, {}});
+          ln.sl.phase_off = (int64_t)C->phases.size();
+          ln.sl.ops_off = (int64_t)C->ops.size();
+          ln.sl.nphase = (int)groups.size();
+          for (auto &gr : groups) {
+            int rm = gr.first;
+            // fill with the highest free tile bits (keeps low bits as lane bits)
+            for (int b = K_ - 1; b >= 0 && popc((u64)rm) < RB; b--) rm |= 1 << b;
+            ShmPhase ph{};
+            int ri = 0;
+            int reg_index[16];
+            for (int b = 0; b < K_; b++) {
+              reg_index[b] = -1;
+              if ((rm >> b) & 1) {
+                ph.rbit[ri] = b;
+                reg_index[b] = ri++;
+              }
+            }
+            for (int i = ri; i < 4; i++) ph.rbit[i] = 0;
+            ph.op_begin = (int32_t)(C->ops.size() - ln.sl.ops_off);
+            for (int i : gr.second) {
+              ShmOp op = pre[i].op;
+              if (pre[i].nt >= 1) op.t0 = reg_index[pre[i].ttile[0]];
+              if (pre[i].nt >= 2) op.t1 = reg_index[pre[i].ttile[1]];
+              for (int a = 0; a < op.nsel; a++) {
+                int slot = pre[i].sel_slot[a];
+                int tb = tile_of_slot[slot];
+                if (tb < 0) {
+                  op.sel_src[a] = SEL_BASE;
+                  op.sel_idx[a] = slot;
+                } else if (reg_index[tb] >= 0) {
+                  op.sel_src[a] = SEL_REG;
+                  op.sel_idx[a] = reg_index[tb];
+                } else {
+                  op.sel_src[a] = SEL_THR;
+                  op.sel_idx[a] = tb;
+                }
+              }
+              C->ops.push_back(op);
+            }
+            ph.op_end = (int32_t)(C->ops.size() - ln.sl.ops_off);
+            C->phases.push_back(ph);
+          }
+        }
+        C->prog[sl].push_back(ln);
+      }
+      if (!scalar_done) {
+        Launch ln;
+        ln.type = L_SCALE;
+        ln.stage = k;
+        ln.sre = scalar[sl].real();
+        ln.sim = scalar[sl].imag();
+        ln.bytes = pass_bytes;
+        C->prog[sl].push_back(ln);
+      }
+    }
+  }
+  C->planned = true;
+  C->blobs_ready = false;
+  C->plan_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ------------------------------------------------------------------ JSON
+static void jmask(std::ostringstream &o, u64 m) {
+  o << "[";
+  bool first = true;
+  for (int q = 0; q < 64; q++)
+    if ((m >> q) & 1) {
+      if (!first) o << ",";
+      o << q;
+      first = false;
+    }
+  o << "]";
+}
+
+std::string plan_json(const atlas_ctx *C) {
+  std::ostringstream o;
+  o << "{\"n\":" << C->n << ",\"L\":" << C->L << ",\"G\":" << C->G << ",\"R\":0"
+    << ",\"c\":" << C->c << ",\"dtype\":\"" << (C->dt == ATLAS_C128 ? "c128" : "c64") << "\""
+    << ",\"staging\":{\"s\":" << C->sp.s << ",\"cost\":" << C->sp.cost
+    << ",\"exact\":" << (C->sp.exact ? "true" : "false") << ",\"gate_stage\":[";
+  for (size_t g = 0; g < C->sp.gate_stage.size(); g++) o << (g ? "," : "") << C->sp.gate_stage[g];
+  o << "]},\"cost_model\":\"" << C->cm.source << "\",\"K_tile\":" << C->K_tile
+    << ",\"ls_qubits\":" << C->cm.ls_qubits << ",\"stages\":[";
+  for (int k = 0; k < C->sp.s; k++) {
+    if (k) o << ",";
+    o << "{\"local\":";
+    jmask(o, C->sp.local[k]);
+    o << ",\"global\":";
+    jmask(o, C->sp.global[k]);
+    o << ",\"sigma\":[";
+    for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].sigma[q];
+    o << "],\"packed\":" << (k > 0 && C->exch[k].packed ? "true" : "false");
+    o << ",\"gates\":[";
+    for (size_t i = 0; i < C->stage_gates[k].size(); i++) o << (i ? "," : "") << C->stage_gates[k][i];
+    o << "],\"kernel_cost\":" << C->kplans[k].total << ",\"kernels\":[";
+    for (size_t i = 0; i < C->kplans[k].kernels.size(); i++) {
+      const Kernel &K = C->kplans[k].kernels[i];
+      if (i) o << ",";
+      o << "{\"kind\":\"" << (K.kind == K_FUSION ? "fusion" : "shm") << "\",\"cost\":" << K.cost
+        << ",\"qubits\":";
+      jmask(o, K.qubits);
+      o << ",\"gates\":[";
+      for (size_t j = 0; j < K.gates.size(); j++) o << (j ? "," : "") << K.gates[j];
+      o << "]}";
+    }
+    o << "]}";
+  }
+  o << "],\"plan_us\":" << C->plan_us << "}";
+  return o.str();
+}
+
+}  // namespace atlas

@@ -1,0 +1,418 @@
+// runtime.cu -- Execute (Alg. 1) and the C-ABI.
+//
+// Per stage: Shard (the inter-stage remap: optional local bit-permutation
+// "pack", then the all-to-all exchange of contiguous blocks -- NCCL grouped
+// send/recv over NVLink, or device copies in virtual-world mode) followed by
+// LaunchKernel for every kernel of the stage on this rank's 2^L shard
+// ("ParFor shard": every rank runs its own shard; no collective
+// inside a stage).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "ctx.h"
+
+namespace atlas {
+
+void build_plan(atlas_ctx *C, int s_max, double cf);
+std::string plan_json(const atlas_ctx *C);
+cudaError_t launch_fused(int dtype, void *st, int L, const FusedLaunch &fl, const double2 *mats,
+                         cudaStream_t s);
+cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const uint64_t *ht,
+                       const ShmOp *ops, const ShmPhase *ph, cudaStream_t s);
+cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const int *newpos_host,
+                           const int *newpos_dev, cudaStream_t s);
+cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
+cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) fail(ATLAS_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_));       \
+  } while (0)
+
+// ------------------------------------------------------------------- NCCL
+// libnccl.so.2 is loaded at run time (torch ships NCCL 2.28); only the few
+// entry points the remap needs are bound.
+struct NcclApi {
+  void *h = nullptr;
+  int (*getUniqueId)(void *) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
+  int (*send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*commDestroy)(void *) = nullptr;
+  const char *(*errStr)(int) = nullptr;
+  void *commInitRank = nullptr;
+};
+struct Uid {
+  char internal[128];
+};
+static NcclApi g_nccl;
+static std::mutex g_nccl_mu;
+
+void nccl_load() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.h) return;
+  const char *names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char *nm : names) {
+    g_nccl.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.h) break;
+  }
+  if (!g_nccl.h) fail(ATLAS_E_NCCL, "cannot load libnccl.so.2: %s", dlerror());
+  g_nccl.getUniqueId = (int (*)(void *))dlsym(g_nccl.h, "ncclGetUniqueId");
+  g_nccl.groupStart = (int (*)())dlsym(g_nccl.h, "ncclGroupStart");
+  g_nccl.groupEnd = (int (*)())dlsym(g_nccl.h, "ncclGroupEnd");
+  g_nccl.send = (int (*)(const void *, size_t, int, int, void *, cudaStream_t))dlsym(g_nccl.h, "ncclSend");
+  g_nccl.recv = (int (*)(void *, size_t, int, int, void *, cudaStream_t))dlsym(g_nccl.h, "ncclRecv");
+  g_nccl.commDestroy = (int (*)(void *))dlsym(g_nccl.h, "ncclCommDestroy");
+  g_nccl.errStr = (const char *(*)(int))dlsym(g_nccl.h, "ncclGetErrorString");
+  g_nccl.commInitRank = dlsym(g_nccl.h, "ncclCommInitRank");
+  if (!g_nccl.getUniqueId || !g_nccl.groupStart || !g_nccl.groupEnd || !g_nccl.send ||
+      !g_nccl.recv || !g_nccl.commInitRank)
+    fail(ATLAS_E_NCCL, "libnccl.so.2 lacks required symbols");
+}
+
+#define NK(x)                                                                         \
+  do {                                                                                \
+    int r_ = (x);                                                                     \
+    if (r_ != 0)                                                                      \
+      fail(ATLAS_E_NCCL, "%s: %s", #x, g_nccl.errStr ? g_nccl.errStr(r_) : "error");  \
+  } while (0)
+
+static const int kNcclUint8 = 1;  // ncclUint8 (nccl.h)
+
+// ---------------------------------------------------------------- device
+static size_t amp_bytes(const atlas_ctx *C) { return C->dt == ATLAS_C128 ? 16 : 8; }
+static size_t shard_bytes(const atlas_ctx *C) { return amp_bytes(C) << C->L; }
+
+void ensure_device(atlas_ctx *C) {
+  if (C->dev_ready) return;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) fail(ATLAS_E_CUDA, "no CUDA device available");
+  if (C->opt.device >= 0) C->device = C->opt.device;
+  else CK(cudaGetDevice(&C->device));
+  CK(cudaSetDevice(C->device));
+  if (!C->stream) {
+    CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
+    C->own_stream = true;
+  }
+  const int slots = C->nslots;
+  C->cur.assign(slots, 0);
+  if (!C->bound) {
+    C->d_state.assign(slots, nullptr);
+    C->d_scratch.assign(slots, nullptr);
+    const size_t b = shard_bytes(C);
+    for (int s = 0; s < slots; s++) {
+      if (cudaMalloc(&C->d_state[s], b) != cudaSuccess)
+        fail(ATLAS_E_OOM, "cudaMalloc(%zu) state failed", b);
+      if (C->world > 1 && cudaMalloc(&C->d_scratch[s], b) != cudaSuccess)
+        fail(ATLAS_E_OOM, "cudaMalloc(%zu) scratch failed", b);
+    }
+  }
+  if (C->world > 1 && !C->opt.virtual_world && !C->nccl_comm) {
+    nccl_load();
+    if (!C->have_uid) fail(ATLAS_E_INVALID, "world > 1 needs an nccl_uid (or virtual_world)");
+    Uid u;
+    memcpy(u.internal, C->nccl_uid, 128);
+    auto init = (int (*)(void **, int, Uid, int))g_nccl.commInitRank;
+    NK(init(&C->nccl_comm, C->world, u, C->rank));
+  }
+  C->dev_ready = true;
+}
+
+template <typename T>
+static void upload(void *&d, const std::vector<T> &v) {
+  if (d) cudaFree(d);
+  d = nullptr;
+  size_t b = std::max<size_t>(v.size(), 1) * sizeof(T);
+  CK(cudaMalloc(&d, b));
+  if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+static void ensure_blobs(atlas_ctx *C) {
+  if (C->blobs_ready) return;
+  upload(C->d_hightab, C->hightab);
+  upload(C->d_ops, C->ops);
+  upload(C->d_phases, C->phases);
+  upload(C->d_mats, C->mats);
+  upload(C->d_newpos, C->newpos);
+  C->blobs_ready = true;
+}
+
+static void *cur_buf(atlas_ctx *C, int s) { return C->cur[s] ? C->d_scratch[s] : C->d_state[s]; }
+static void *other_buf(atlas_ctx *C, int s) { return C->cur[s] ? C->d_state[s] : C->d_scratch[s]; }
+
+// sizes of the simulated ranks' world (virtual mode: slot == rank)
+static int slot_rank(const atlas_ctx *C, int s) { return C->nslots > 1 ? s : C->rank; }
+
+// Exchange of stage k (after the optional pack) for all local slots.
+static void do_exchange(atlas_ctx *C, int k) {
+  const Exchange &ex = C->exch[k];
+  const int gp = ex.gp;
+  const size_t blk = amp_bytes(C) << (C->L - gp);
+  const int nb = 1 << gp;
+  u64 Gam = 0;
+  for (int j = 0; j < gp; j++) Gam |= 1ull << ex.gamma[j];
+  auto dest = [&](int r, int b, int *rdst, int *beta) {
+    int rd = (int)(r & ~Gam);
+    int bt = 0;
+    for (int j = 0; j < gp; j++) {
+      rd |= ((b >> j) & 1) << ex.gamma[j];
+      bt |= (((r >> ex.gamma[j]) & 1) ^ ex.fI[j]) << j;
+    }
+    *rdst = rd;
+    *beta = bt;
+  };
+  if (C->nslots > 1) {
+    // virtual world: all shards on this device
+    for (int r = 0; r < C->nslots; r++) {
+      const char *src = (const char *)cur_buf(C, r);
+      for (int b = 0; b < nb; b++) {
+        int rd, bt;
+        dest(r, b, &rd, &bt);
+        char *dst = (char *)other_buf(C, rd);
+        CK(cudaMemcpyAsync(dst + (size_t)bt * blk, src + (size_t)b * blk, blk,
+                           cudaMemcpyDeviceToDevice, C->stream));
+      }
+    }
+    for (int r = 0; r < C->nslots; r++) C->cur[r] ^= 1;
+    return;
+  }
+  if (C->world == 1) return;
+  const int r = C->rank;
+  const char *src = (const char *)cur_buf(C, 0);
+  char *dst = (char *)other_buf(C, 0);
+  // every peer p of my group sends me its block b = my bits at gamma; that
+  // block lands at beta(p) -- so I receive from p into dst + beta(p) * blk.
+  NK(g_nccl.groupStart());
+  for (int b = 0; b < nb; b++) {
+    int rd, bt;
+    dest(r, b, &rd, &bt);
+    if (rd == r) {
+      CK(cudaMemcpyAsync(dst + (size_t)bt * blk, src + (size_t)b * blk, blk,
+                         cudaMemcpyDeviceToDevice, C->stream));
+      continue;
+    }
+    NK(g_nccl.send(src + (size_t)b * blk, blk, kNcclUint8, rd, C->nccl_comm, C->stream));
+  }
+  for (int pb = 0; pb < nb; pb++) {
+    // peer p: r with gamma bits replaced by pb
+    int p = (int)(r & ~Gam);
+    for (int j = 0; j < gp; j++) p |= ((pb >> j) & 1) << ex.gamma[j];
+    if (p == r) continue;
+    int myb = 0;  // the block index p sends me = my gamma bits
+    for (int j = 0; j < gp; j++) myb |= ((r >> ex.gamma[j]) & 1) << j;
+    int rd, bt;
+    dest(p, myb, &rd, &bt);
+    NK(g_nccl.recv(dst + (size_t)bt * blk, blk, kNcclUint8, p, C->nccl_comm, C->stream));
+  }
+  NK(g_nccl.groupEnd());
+  C->cur[0] ^= 1;
+}
+
+void run(atlas_ctx *C) {
+  if (!C->planned) fail(ATLAS_E_ORDER, "atlas_run before atlas_plan");
+  ensure_device(C);
+  ensure_blobs(C);
+  const int dt = C->dt == ATLAS_C128 ? 0 : 1;
+  const bool timing = C->opt.timing != 0;
+  C->launch_ms.clear();
+  C->launch_kind.clear();
+  C->launch_bytes.clear();
+  std::vector<std::pair<int, int64_t>> rec;  // kind, bytes
+  size_t nev = 0;
+  auto ev_at = [&](size_t i) {
+    while (C->ev.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      C->ev.push_back(e);
+    }
+    return C->ev[i];
+  };
+  auto mark = [&](int kind, int64_t bytes) {
+    if (!timing) return;
+    CK(cudaEventRecord(ev_at(nev++), C->stream));
+    rec.push_back({kind, bytes});
+  };
+  auto mark_end = [&]() {
+    if (timing) CK(cudaEventRecord(ev_at(nev++), C->stream));
+  };
+  // init |0...0>: logical 0 -> physical 0 (no flips at stage 0) on rank 0
+  for (int s = 0; s < C->nslots; s++) {
+    if (!C->opt.init && C->state_set) continue;
+    C->cur[s] = 0;
+    mark(L_INIT, (int64_t)shard_bytes(C));
+    CK(launch_init(dt, cur_buf(C, s), C->L, slot_rank(C, s) == 0, C->stream));
+    mark_end();
+  }
+  if (!C->opt.init && !C->state_set) fail(ATLAS_E_ORDER, "option init=0 but no atlas_set_state");
+  C->state_set = false;
+  const int S = C->sp.s;
+  std::vector<size_t> pc(C->nslots, 0);
+  const double2 *mats = (const double2 *)C->d_mats;
+  for (int k = 0; k < S; k++) {
+    // remap: pack (per slot), then exchange (all slots together)
+    if (k > 0 && C->exch[k].gp > 0) {
+      for (int s = 0; s < C->nslots; s++) {
+        auto &P = C->prog[s];
+        while (pc[s] < P.size() && P[pc[s]].stage == k && P[pc[s]].type == L_PACK) {
+          const Launch &ln = P[pc[s]++];
+          mark(L_PACK, ln.bytes);
+          CK(launch_permute(dt, cur_buf(C, s), other_buf(C, s), C->L, &C->newpos[ln.newpos_off],
+                            (const int *)C->d_newpos + ln.newpos_off, C->stream));
+          mark_end();
+          C->cur[s] ^= 1;
+        }
+        if (pc[s] < P.size() && P[pc[s]].stage == k && P[pc[s]].type == L_EXCHANGE) pc[s]++;
+      }
+      mark(L_EXCHANGE, C->prog[0].empty() ? 0 : (int64_t)((double)shard_bytes(C) * (1.0 - std::ldexp(1.0, -C->exch[k].gp))) * C->nslots);
+      do_exchange(C, k);
+      mark_end();
+    }
+    for (int s = 0; s < C->nslots; s++) {
+      auto &P = C->prog[s];
+      while (pc[s] < P.size() && P[pc[s]].stage == k) {
+        const Launch &ln = P[pc[s]++];
+        void *st = cur_buf(C, s);
+        mark(ln.type, ln.bytes);
+        switch (ln.type) {
+          case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
+          case L_SHM:
+            CK(launch_shm(dt, st, ln.sl, (const uint64_t *)C->d_hightab, (const ShmOp *)C->d_ops,
+                          (const ShmPhase *)C->d_phases, C->stream));
+            break;
+          case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;
+          default: fail(ATLAS_E_INVALID, "internal: unexpected launch type %d", ln.type);
+        }
+        mark_end();
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(C->stream));
+  if (timing) {
+    for (size_t i = 0; i < rec.size(); i++) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, C->ev[2 * i], C->ev[2 * i + 1]));
+      C->launch_ms.push_back(ms);
+      C->launch_kind.push_back(rec[i].first);
+      C->launch_bytes.push_back(rec[i].second);
+    }
+  }
+}
+
+// logical index -> (rank, offset) in the last stage's layout
+static void locate(const atlas_ctx *C, int stage, uint64_t x, int *rank, uint64_t *off) {
+  const StageMap &mp = C->maps[stage];
+  const std::vector<int> &fl = stage == C->sp.s - 1 ? mp.flip_end : mp.flip_begin;
+  uint64_t p = 0;
+  for (int q = 0; q < C->n; q++) {
+    uint64_t b = ((x >> q) & 1) ^ (uint64_t)fl[q];
+    p |= b << mp.sigma[q];
+  }
+  *rank = (int)(p >> C->L);
+  *off = p & ((1ull << C->L) - 1);
+}
+
+static bool identity_layout(const atlas_ctx *C, int stage, bool end) {
+  const StageMap &mp = C->maps[stage];
+  const std::vector<int> &fl = end ? mp.flip_end : mp.flip_begin;
+  for (int q = 0; q < C->n; q++)
+    if (mp.sigma[q] != q || fl[q]) return false;
+  return true;
+}
+
+void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
+  if (!C->planned || !C->dev_ready) fail(ATLAS_E_ORDER, "atlas_get_state before atlas_run");
+  if (count == 0) return;
+  if (first + count > (1ull << C->n) || first + count < first) fail(ATLAS_E_INVALID, "range out of bounds");
+  const size_t B = amp_bytes(C);
+  const int last = C->sp.s - 1;
+  CK(cudaSetDevice(C->device));
+  if (identity_layout(C, last, true)) {
+    // physical == logical: contiguous copies per shard
+    uint64_t x = first, end = first + count;
+    while (x < end) {
+      int r = (int)(x >> C->L);
+      uint64_t off = x & ((1ull << C->L) - 1);
+      uint64_t len = std::min<uint64_t>(end - x, (1ull << C->L) - off);
+      int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
+      if (s >= 0)
+        CK(cudaMemcpy((char *)host + (x - first) * B, (const char *)cur_buf(C, s) + off * B, len * B,
+                      cudaMemcpyDeviceToHost));
+      x += len;
+    }
+    return;
+  }
+  // general layout: bring the shard(s) to the host and gather
+  std::vector<std::vector<char>> sh(C->nslots);
+  for (int s = 0; s < C->nslots; s++) {
+    sh[s].resize(shard_bytes(C));
+    CK(cudaMemcpy(sh[s].data(), cur_buf(C, s), shard_bytes(C), cudaMemcpyDeviceToHost));
+  }
+  for (uint64_t i = 0; i < count; i++) {
+    int r;
+    uint64_t off;
+    locate(C, last, first + i, &r, &off);
+    int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
+    if (s < 0) continue;
+    memcpy((char *)host + i * B, sh[s].data() + off * B, B);
+  }
+}
+
+void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
+  if (!C->planned) fail(ATLAS_E_ORDER, "atlas_set_state before atlas_plan");
+  if (first + count > (1ull << C->n)) fail(ATLAS_E_INVALID, "range out of bounds");
+  ensure_device(C);
+  const size_t B = amp_bytes(C);
+  for (int s = 0; s < C->nslots; s++) C->cur[s] = 0;
+  // stage-0 layout has no flips
+  std::vector<std::vector<char>> sh(C->nslots);
+  for (int s = 0; s < C->nslots; s++) {
+    sh[s].resize(shard_bytes(C));
+    CK(cudaMemcpy(sh[s].data(), C->d_state[s], shard_bytes(C), cudaMemcpyDeviceToHost));
+  }
+  for (uint64_t i = 0; i < count; i++) {
+    int r;
+    uint64_t off;
+    locate(C, 0, first + i, &r, &off);
+    int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
+    if (s < 0) continue;
+    memcpy(sh[s].data() + off * B, (const char *)host + i * B, B);
+  }
+  for (int s = 0; s < C->nslots; s++)
+    CK(cudaMemcpy(C->d_state[s], sh[s].data(), shard_bytes(C), cudaMemcpyHostToDevice));
+  C->state_set = true;
+}
+
+void destroy(atlas_ctx *C) {
+  if (C->dev_ready) {
+    cudaSetDevice(C->device);
+    cudaStreamSynchronize(C->stream);
+    if (!C->bound)
+      for (size_t s = 0; s < C->d_state.size(); s++) {
+        if (C->d_state[s]) cudaFree(C->d_state[s]);
+        if (C->d_scratch[s]) cudaFree(C->d_scratch[s]);
+      }
+    for (void *p : {C->d_hightab, C->d_ops, C->d_phases, C->d_mats, C->d_newpos})
+      if (p) cudaFree(p);
+    for (auto e : C->ev) cudaEventDestroy(e);
+    if (C->own_stream) cudaStreamDestroy(C->stream);
+    if (C->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(C->nccl_comm);
+  }
+  delete C;
+}
+
+
+
+void nccl_unique_id(void *out) {
+  nccl_load();
+  NK(g_nccl.getUniqueId(out));
+}
+
+}  // namespace atlas

@@ -1,0 +1,122 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle O1,
+element by element on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): fp64 max|d amp| <= 1e-10 and
+1 - F <= 1e-9; fp32 1e-4 and 1e-5.  No global-phase alignment.
+"""
+import numpy as np
+import pytest
+
+from oracle import sim as O
+from workloads import circuits as C
+
+pytestmark = pytest.mark.gpu
+
+A = pytest.importorskip("paper_2408_09055_b200.atlas")
+
+TOL = {0: (1e-10, 1e-9), 1: (1e-4, 1e-5)}
+
+
+def fidelity(a, b):
+    a = a.astype(np.complex128)
+    b = b.astype(np.complex128)
+    return abs(np.vdot(a, b)) ** 2 / (np.vdot(a, a).real * np.vdot(b, b).real)
+
+
+def check(psi_gpu, psi_ref, dtype=0):
+    md, fd = TOL[dtype]
+    d = np.abs(psi_gpu.astype(np.complex128) - psi_ref).max()
+    f = 1 - fidelity(psi_gpu, psi_ref)
+    assert d <= md, f"max|d|={d:.3e}"
+    assert f <= fd, f"1-F={f:.3e}"
+    return d, f
+
+
+def run(c, dtype=0, world=1, init=None, **opt):
+    with A.Simulator(c.n, dtype, world, 0, virtual_world=1 if world > 1 else 0, **opt) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        if init is not None:
+            s.set_option("init", 0)
+            s.set_state(init)
+        s.run()
+        return s.get_state(), s.plan_json()
+
+
+def test_qft12_config1():
+    """BASELINE config 1: qft n=12 fp64, single stage, 1 GPU vs the oracle."""
+    c = C.qft(12)
+    psi, plan = run(c)
+    assert plan["staging"]["s"] == 1
+    check(psi, O.simulate(c))
+
+
+@pytest.mark.parametrize("fam", C.FAMILIES)
+@pytest.mark.parametrize("n", [13, 18])
+def test_families_world1(fam, n):
+    c = C.make(fam, n)
+    psi, _ = run(c)
+    check(psi, O.simulate(c))
+
+
+@pytest.mark.parametrize("kernelizer", [0, 1, 2])
+@pytest.mark.parametrize("kinds", [1, 2, 3])
+def test_kernel_kinds(kernelizer, kinds):
+    if kernelizer == 2 and kinds == 2:
+        pytest.skip("greedy baseline is fusion-only")
+    c = C.su2random(14)
+    psi, plan = run(c, kernelizer=kernelizer, kinds=kinds)
+    check(psi, O.simulate(c))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_circuits_random_input(seed):
+    """Arbitrary input states and every gate kind."""
+    n = 12 + seed % 4
+    c = C.random_circuit(n, 120, seed)
+    rng = np.random.default_rng(seed)
+    psi0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    psi, _ = run(c, init=psi0)
+    check(psi, O.simulate(c, init=psi0))
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+@pytest.mark.parametrize("fam", ["qft", "ghz", "su2random", "ising", "wstate"])
+def test_virtual_world(fam, W):
+    """W > 1 plans (staging + remaps + per-rank insular specialisation) run
+    with all ranks' shards on one GPU."""
+    c = C.make(fam, 14)
+    psi, plan = run(c, world=W)
+    check(psi, O.simulate(c))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_virtual_world_random(seed):
+    n = 12
+    c = C.random_circuit(n, 80, 50 + seed)
+    psi, plan = run(c, world=4)
+    check(psi, O.simulate(c))
+
+
+@pytest.mark.parametrize("fam", ["qft", "su2random", "ghz"])
+def test_fp32(fam):
+    c = C.make(fam, 16)
+    psi, _ = run(c, dtype=1)
+    check(psi, O.simulate(c), dtype=1)
+
+
+def test_ls_qubits_paper_setting():
+    """The paper forces 3 LSB qubits into shared-memory kernels."""
+    c = C.qsvm(15)
+    psi, plan = run(c, ls_qubits=3)
+    check(psi, O.simulate(c))
+
+
+def test_tile_sizes():
+    c = C.ising(16)
+    ref = O.simulate(c)
+    for k in (6, 8, 10, 11, 13):
+        psi, plan = run(c, shm_qubits=k)
+        assert plan["K_tile"] == k
+        check(psi, ref)
