@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""bench.py -- Atlas hot path on B200: circuit simulation time and
+amplitude-updates/s (BASELINE.json metric), with roofline, CPU-oracle baseline,
+end-to-end (host buffers) number and clock record.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload su2random_n28]
+                  [--impl reference]
+
+A *step* is one full simulation of the workload circuit through the C-ABI
+(atlas_run: |0...0> initialisation, every stage's kernels, every inter-stage
+remap).  N=1 runs BASELINE config 2 (su2random, n=28, fp64, one B200).  Under
+torchrun with N>1 ranks the run is weak-scaled like the paper's E1 (28 local
+qubits per GPU, n = 28 + log2 N) with NCCL remaps between
+stages; the timed region is max over ranks.
+
+value   = m * 2^n / T_step  (gate-level amplitude updates per second, SURVEY
+          Q24), whole job.
+e2e     = same metric through the public API with host buffers: load circuit
+          from host, plan, run, read the whole final state into pinned host
+          memory every step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import circuits as C  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--workload", default="su2random_n28")
+    p.add_argument("--impl", default="atlas", choices=["atlas", "reference"])
+    p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--kernelizer", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--opt", action="append", default=[], help="extra library option key=int")
+    return p.parse_args()
+
+
+def workload(name, world):
+    fam, nstr = name.rsplit("_n", 1)
+    n = int(nstr)
+    if world > 1:
+        n += int(math.log2(world))  # weak scaling: 28 local qubits per GPU
+    return C.make(fam, n), fam, n
+
+
+# ---------------------------------------------------------------- clocks
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                s = float(f[0])
+                mx = float(f[1])
+            except ValueError:
+                continue
+            sm.append(s)
+            for name, v in zip(REASONS, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
+        load = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU oracle
+def cpu_oracle_sample(circ, budget_s=12.0, max_gates=None):
+    """Time the oracle (as it stands) on the first g gates of the workload
+    at full n, single thread.  Returns (updates/s, g, seconds)."""
+    from oracle import sim as O
+    import numpy as np
+    n = circ.n
+    g = 1
+    # calibrate on one gate
+    t0 = time.perf_counter()
+    O.simulate(C.Circuit(n, circ.gates[:1]))
+    t1 = time.perf_counter() - t0
+    per_gate = max(t1 * 0.8, 1e-6)  # includes the |0> init, so an upper bound
+    g = max(1, min(len(circ.gates), int(budget_s / per_gate)))
+    if max_gates:
+        g = min(g, max_gates)
+    t0 = time.perf_counter()
+    O.simulate(C.Circuit(n, circ.gates[:g]))
+    dt = time.perf_counter() - t0
+    return g * (2.0 ** n) / dt, g, dt
+
+
+def load_peaks():
+    try:
+        d = json.load(open(PEAKS_FILE))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------- reference
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    circ, fam, n = workload(args.workload, args.gpus)
+    from oracle import sim as O
+    O.build()
+    vals = []
+    per = None
+    for i in range(args.warmup + args.steps):
+        v, g, dt = cpu_oracle_sample(circ, budget_s=6.0, max_gates=per)
+        per = g
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.median(dt for _, dt in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": "amplitude-updates/s (circuit simulation)",
+        "value": value, "unit": "amp-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{fam}_n{n}_fp64", "n": n, "gates": len(circ.gates),
+                   "sample_gates_per_step": per},
+        "cpu_baseline": {"value": value, "unit": "amp-updates/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {per} of {len(circ.gates)} gates of {fam} n={n} "
+                                   f"(complex128, gate-at-a-time C oracle) per step"},
+        "e2e": {"value": value, "unit": "amp-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- atlas
+def run_atlas(args):
+    import numpy as np
+    import torch
+    from paper_2408_09055_b200 import atlas as A
+
+    world = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        assert dist.get_world_size() == world
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    circ, fam, n = workload(args.workload, world)
+    dtype = A.C128 if args.dtype == "f64" else A.C64
+    uid = None
+    if world > 1:
+        obj = [A.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.Stream()
+    extra = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.opt}
+    sim = A.Simulator(n, dtype, world, rank, uid, kernelizer=args.kernelizer, device=dev, **extra)
+    sim.set_stream(stream.cuda_stream)
+    t0 = time.perf_counter()
+    sim.load_circuit(circ.gates)
+    sim.plan(16, 3.0)
+    plan_s = time.perf_counter() - t0
+    stats = sim.plan_stats()
+    m = len(circ.gates)
+    updates = m * float(2 ** n)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up (uploads the plan, allocates the shard)
+    for _ in range(args.warmup):
+        sim.run()
+    torch.cuda.synchronize()
+    sim.set_option("timing", 1)
+    launches = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            sim.run()
+            launches.extend(sim.launches())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = updates / (ms_step / 1e3)
+    sim.set_option("timing", 0)
+
+    # roofline: dominant kernel kind by total device time
+    by = {}
+    for kind, t, b in launches:
+        if kind not in ("fused", "shm", "pack", "scale"):
+            continue
+        d = by.setdefault(kind, [0.0, 0, 0])
+        d[0] += t
+        d[1] += 1
+        d[2] += b
+    step_kernel_ms = sum(v[0] for v in by.values()) / args.steps
+    dom = max(by, key=lambda k: by[k][0]) if by else None
+    peak, peak_src = load_peaks()
+    roof = None
+    if dom:
+        tot_ms, cnt, byts = by[dom]
+        avg_ms = tot_ms / cnt
+        bytes_per = byts / cnt
+        ach = bytes_per / (avg_ms / 1e3) / 1e9
+        traffic = load_traffic().get(f"{dom}_{args.workload}_{args.dtype}")
+        roof = {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": round(ach, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": traffic, "peak_source": peak_src,
+                "launches_per_step": cnt / args.steps, "avg_launch_ms": round(avg_ms, 4),
+                "share_of_step": round(tot_ms / args.steps / ms_step, 4),
+                "bytes_per_launch": int(bytes_per)}
+    kinds_ms = {k: round(v[0] / args.steps, 4) for k, v in by.items()}
+    remap_ms = sum(t for k, t, b in launches if k == "exchange") / args.steps
+    n_launch = sum(1 for k, t, b in launches if k in ("fused", "shm", "pack", "scale", "init"))
+
+    # e2e: host buffers through the public API
+    e2e = None
+    if not args.no_e2e:
+        amp = 16 if dtype == A.C128 else 8
+        count = (1 << sim.n) if world == 1 else (1 << (n - int(math.log2(world))))
+        host = torch.empty(count * amp, dtype=torch.uint8, pin_memory=True)
+        first = 0 if world == 1 else None
+        arr, mg = A.encode_gates(circ.gates)
+        h2d = mg * ctypes.sizeof(A.Gate)
+        reps = max(1, min(3, args.steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            sim.load_circuit(circ.gates)
+            sim.plan(16, 3.0)
+            sim.run()
+            if world == 1:
+                sim.get_state_into(host.data_ptr(), 0, count)
+            else:
+                sim.get_state_into(host.data_ptr(), 0, 1)  # rank-local read of the result
+        dt = (time.perf_counter() - t0) / reps
+        if dist is not None:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": updates / dt, "unit": "amp-updates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(count * amp if world == 1 else amp),
+               "ms_per_step": round(dt * 1e3, 3),
+               "includes": "load_circuit + plan + run + get_state(full state -> pinned host)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, g, dt = cpu_oracle_sample(circ, budget_s=12.0)
+        cpu = {"value": v, "unit": "amp-updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {g} of {m} gates of {fam} n={n} at full size, "
+                         f"complex128 gate-at-a-time C oracle, 1 thread, {dt:.1f} s"}
+    sim.close()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    pj = {"stages": stats["stages"], "remaps": stats["remaps"], "kernels": stats["kernels"],
+          "fusion_kernels": stats["fusion_kernels"], "shm_kernels": stats["shm_kernels"],
+          "plan_s": round(plan_s, 3), "staging_exact": bool(stats["staging_exact"])}
+    line = {
+        "metric": "amplitude-updates/s (circuit simulation)",
+        "value": value, "unit": "amp-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"{fam}_n{n}_{'fp64' if dtype == A.C128 else 'fp32'}",
+                   "n": n, "gates": m, "L": stats["L"], "G": stats["G"],
+                   "parallelism": f"state sharded over {world} GPU(s), NCCL remaps",
+                   "l2": "state (%.0f GiB/GPU) >> L2; no flush needed" % ((16 if dtype == A.C128 else 8) * 2 ** (n - int(math.log2(world))) / 2 ** 30),
+                   "plan": pj, "kernel_ms_per_step": kinds_ms,
+                   "remap_ms_per_step": round(remap_ms, 4),
+                   "kernels_ms_per_step_total": round(step_kernel_ms, 4)},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": n_launch,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_atlas(args)
+
+
+if __name__ == "__main__":
+    main()

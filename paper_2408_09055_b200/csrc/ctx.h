@@ -51,6 +51,7 @@ struct Options {
   int timing = 0;
   int device = -1;
   long stage_budget = 2000000;
+  int shm_nbuf = 1;
   std::string cost_model;
 };
 
@@ -83,7 +84,7 @@ struct atlas_ctx {
   // lowered programs: one per simulated rank (world in virtual mode, else 1)
   int nslots = 1;
   std::vector<std::vector<atlas::Launch>> prog;
-  std::vector<uint64_t> hightab;
+  std::vector<double> coef;
   std::vector<atlas::ShmOp> ops;
   std::vector<atlas::ShmPhase> phases;
   std::vector<double2> mats;
@@ -97,7 +98,7 @@ struct atlas_ctx {
   std::vector<void *> d_state, d_scratch;  // per slot
   std::vector<int> cur;                    // 0: state holds the data, 1: scratch
   bool bound = false;
-  void *d_hightab = nullptr, *d_ops = nullptr, *d_phases = nullptr, *d_mats = nullptr,
+  void *d_coef = nullptr, *d_ops = nullptr, *d_phases = nullptr, *d_mats = nullptr,
        *d_newpos = nullptr;
   std::vector<cudaEvent_t> ev;
   std::vector<float> launch_ms;

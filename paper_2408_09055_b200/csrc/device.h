@@ -18,40 +18,39 @@ namespace atlas {
 // is known per tile ("converts these gates into smaller gates with
 // only active qubits").
 // ----------------------------------------------------------------------------
-enum ShmOpType : int32_t {
-  OP_DIAG = 0,   // multiply by ph[sel]           (no target)
-  OP_DENSE1 = 1, // 2x2 block on register bit t0, applied where sel == selv
-  OP_PERM1 = 2,  // swap pair on register bit t0 (X-type), where sel == selv
-  OP_DENSE2 = 3, // 4x4 block on register bits (t0 = low, t1 = high), sel == selv
+enum ShmOpType : uint8_t {
+  OP_PHASE = 0,   // v[e] *= c                      (diagonal gates, scalars)
+  OP_DENSE1 = 1,  // 2x2 block on register bit t0
+  OP_PERM1 = 2,   // swap on register bit t0 (X-type block)
+  OP_DENSE2 = 3,  // 4x4 block on register bits t0 < t1
 };
 
-enum SelSrc : int32_t { SEL_REG = 0, SEL_THR = 1, SEL_BASE = 2 };
-
+// One op of a shared-memory kernel.  It acts on the register elements e with
+// bit e of emask set, in threads whose fixed tile bits
+// satisfy (jt & thr_mask) == thr_val, in tiles whose base satisfies
+// (base & base_mask) == base_val -- i.e. the selector (control / diagonal)
+// values of the gate.
 struct ShmOp {
-  int32_t type;
-  int32_t t0, t1;          // register-bit indices of the targets
-  int32_t nsel;            // number of selector bits (<= 3)
-  int32_t sel_src[3];      // SelSrc
-  int32_t sel_idx[3];      // REG: register bit; THR: tile bit; BASE: physical slot
-  int32_t selv;            // DENSE/PERM: selector value on which the block acts
-  int32_t pad;
-  double m[32];            // DIAG: ph[2^nsel] (re,im); DENSE1: 2x2; DENSE2: 4x4
+  uint8_t type, t0, t1, pad;
+  uint16_t emask;              // register-bit condition as a mask over e (or pair/quad base e)
+  uint16_t pad2;
+  uint16_t thr_mask, thr_val;
+  int32_t coef;                // offset (doubles) into the launch's coefficients
+  uint64_t base_mask, base_val;
 };
+static_assert(sizeof(ShmOp) == 32, "ShmOp layout");
 
 struct ShmPhase {
-  int32_t rbit[4];         // tile bits held in registers (RB used)
+  int32_t rbit[4];             // tile bits held in registers (RB used)
   int32_t op_begin, op_end;
 };
 
 struct ShmLaunch {
-  int32_t K, RB;           // tile bits, register bits
-  int32_t c0;              // leading contiguous active slots (act[i] == i for i < c0)
-  int32_t nphase;
-  uint64_t nonactive;      // mask of non-active local slots (tile base bits)
+  int32_t K, RB, nphase, nops, ncoef, nbuf;  // nbuf: 1 or 2 tile buffers
+  int32_t act[16];             // tile bit b <-> physical slot act[b] (ascending)
+  uint64_t nonactive;          // mask of the non-active local slots
   uint64_t ntiles;
-  int64_t hightab_off;     // offset (elements of uint64) into the table blob
-  int64_t ops_off;         // offset (ShmOp) into the op blob
-  int64_t phase_off;       // offset (ShmPhase) into the phase blob
+  int64_t ops_off, coef_off, phase_off;
 };
 
 // Fused dense kernel ("Fusion"): one 2^k x 2^k matrix on k slots.

@@ -27,6 +27,8 @@ template <> struct Cplx<double> { using T = double2; };
 template <> struct Cplx<float> { using T = float2; };
 
 // ------------------------------------------------------------------ helpers
+__host__ __device__ constexpr int ctz_c(int e) { return (e & 1) ? 0 : 1 + ctz_c(e >> 1); }
+
 __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
   uint64_t r = 0;
   while (mask) {
@@ -41,11 +43,11 @@ __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
 // Swizzle of a tile index so that the 8 (fp64) / 16 (fp32) lanes of one
 // shared-memory wavefront hit distinct 16-byte bank groups for the access
 // patterns of the load/store loops and of most register phases.
-template <typename R> __device__ __forceinline__ int swz(int j);
-template <> __device__ __forceinline__ int swz<double>(int j) {
+template <typename R> __host__ __device__ constexpr int swz(int j);
+template <> __host__ __device__ constexpr int swz<double>(int j) {
   return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7);
 }
-template <> __device__ __forceinline__ int swz<float>(int j) {
+template <> __host__ __device__ constexpr int swz<float>(int j) {
   return j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15);
 }
 
@@ -138,20 +140,27 @@ __global__ void __launch_bounds__(256) fused_kernel(typename Cplx<R>::T *__restr
 }
 
 // ------------------------------------------------------------- shm kernel
-template <typename T, int NE, int TB>
-__device__ __forceinline__ void dense1(T (&v)[NE], const T (&m)[4], int need_mask,
-                                       int need_val, bool fixed_ok) {
+// Register-element loops are fully unrolled: e (and the pair partner) are
+// compile-time, the op's condition is a runtime bit mask over e.  UNI = the
+// op applies in every lane of the warp (no thread-bit selector).
+template <typename T, int NE, int TB, bool UNI>
+__device__ __forceinline__ void dense1(T (&v)[NE], const T (&m)[4], unsigned emask, bool ok) {
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     if (e & (1 << TB)) continue;
     const int e1 = e | (1 << TB);
-    if (fixed_ok && (e & need_mask) == need_val) {
-      T a = v[e], b = v[e1];
+    if ((UNI || ok) && ((emask >> e) & 1u)) {
+      const T a = v[e], b = v[e1];
       T y0, y1;
-      y0.x = 0; y0.y = 0; y1.x = 0; y1.y = 0;
-      cmac(y0, m[0], a);
+      y0.x = m[0].x * a.x;
+      y0.y = m[0].x * a.y;
+      y1.x = m[2].x * a.x;
+      y1.y = m[2].x * a.y;
+      y0.x = fma(-m[0].y, a.y, y0.x);
+      y0.y = fma(m[0].y, a.x, y0.y);
+      y1.x = fma(-m[2].y, a.y, y1.x);
+      y1.y = fma(m[2].y, a.x, y1.y);
       cmac(y0, m[1], b);
-      cmac(y1, m[2], a);
       cmac(y1, m[3], b);
       v[e] = y0;
       v[e1] = y1;
@@ -159,27 +168,27 @@ __device__ __forceinline__ void dense1(T (&v)[NE], const T (&m)[4], int need_mas
   }
 }
 
-template <typename T, int NE, int TB>
-__device__ __forceinline__ void perm1(T (&v)[NE], int need_mask, int need_val, bool fixed_ok) {
+template <typename T, int NE, int TB, bool UNI>
+__device__ __forceinline__ void perm1(T (&v)[NE], unsigned emask, bool ok) {
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     if (e & (1 << TB)) continue;
     const int e1 = e | (1 << TB);
-    if (fixed_ok && (e & need_mask) == need_val) {
-      T a = v[e];
+    if ((UNI || ok) && ((emask >> e) & 1u)) {
+      const T a = v[e];
       v[e] = v[e1];
       v[e1] = a;
     }
   }
 }
 
-template <typename T, int NE, int TB0, int TB1>
-__device__ __forceinline__ void dense2(T (&v)[NE], const double *__restrict__ m, int need_mask,
-                                       int need_val, bool fixed_ok) {
+template <typename T, int NE, int TB0, int TB1, bool UNI>
+__device__ __forceinline__ void dense2(T (&v)[NE], const double *__restrict__ m, unsigned emask,
+                                       bool ok) {
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     if (e & ((1 << TB0) | (1 << TB1))) continue;
-    if (fixed_ok && (e & need_mask) == need_val) {
+    if ((UNI || ok) && ((emask >> e) & 1u)) {
       const int idx[4] = {e, e | (1 << TB0), e | (1 << TB1), e | (1 << TB0) | (1 << TB1)};
       T x[4], y[4];
 #pragma unroll
@@ -202,168 +211,235 @@ __device__ __forceinline__ void dense2(T (&v)[NE], const double *__restrict__ m,
   }
 }
 
-template <typename R, int RB>
-__device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB],
-                                         const ShmOp *__restrict__ op, int jt, uint64_t base) {
+template <typename R, int RB, bool UNI>
+__device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB], const ShmOp &o,
+                                         const double *__restrict__ coef, bool ok) {
   using T = typename Cplx<R>::T;
   constexpr int NE = 1 << RB;
-  const int type = op->type;
-  const int nsel = op->nsel;
-  // Split the selector into its register part (varies per element) and its
-  // fixed part (thread bits of the tile, or non-active bits of the tile base).
-  int reg_mask = 0, reg_bit_of_sel[3] = {0, 0, 0};
-  int fixed = 0, fixed_mask = 0;
-  for (int s = 0; s < nsel; s++) {
-    const int src = op->sel_src[s], idx = op->sel_idx[s];
-    if (src == SEL_REG) {
-      reg_mask |= 1 << idx;
-      reg_bit_of_sel[s] = idx;
-    } else {
-      const int bitv = (src == SEL_THR) ? ((jt >> idx) & 1) : (int)((base >> idx) & 1);
-      fixed |= bitv << s;
-      fixed_mask |= 1 << s;
-    }
-  }
-  if (type == OP_DIAG) {
-    // y = ph[sel] * x; loop over selector values (<= 8)
-    const int nv = 1 << nsel;
-    for (int sv = 0; sv < nv; sv++) {
-      if ((sv & fixed_mask) != fixed) continue;
-      T ph;
-      ph.x = (R)op->m[2 * sv];
-      ph.y = (R)op->m[2 * sv + 1];
-      if (ph.x == (R)1 && ph.y == (R)0) continue;
-      int need = 0;
-      for (int s = 0; s < nsel; s++)
-        if ((reg_mask >> reg_bit_of_sel[s]) & 1 && op->sel_src[s] == SEL_REG)
-          need |= ((sv >> s) & 1) << reg_bit_of_sel[s];
+  const unsigned em = o.emask;
+  switch (o.type) {
+    case OP_PHASE: {
+      T c;
+      c.x = (R)coef[o.coef];
+      c.y = (R)coef[o.coef + 1];
 #pragma unroll
       for (int e = 0; e < NE; e++)
-        if ((e & reg_mask) == need) v[e] = cmul(ph, v[e]);
+        if ((UNI || ok) && ((em >> e) & 1u)) v[e] = cmul(c, v[e]);
+      break;
     }
-    return;
-  }
-  const int selv = op->selv;
-  const bool fixed_ok = (selv & fixed_mask) == fixed;
-  if (!__any_sync(0xffffffffu, fixed_ok)) return;
-  int need = 0;
-  for (int s = 0; s < nsel; s++)
-    if (op->sel_src[s] == SEL_REG) need |= ((selv >> s) & 1) << reg_bit_of_sel[s];
-  const int t0 = op->t0;
-  if (type == OP_PERM1) {
-    switch (t0) {
-      case 0: perm1<T, NE, 0>(v, reg_mask, need, fixed_ok); break;
-      case 1: if (RB > 1) perm1<T, NE, (RB > 1 ? 1 : 0)>(v, reg_mask, need, fixed_ok); break;
-      case 2: if (RB > 2) perm1<T, NE, (RB > 2 ? 2 : 0)>(v, reg_mask, need, fixed_ok); break;
-      case 3: if (RB > 3) perm1<T, NE, (RB > 3 ? 3 : 0)>(v, reg_mask, need, fixed_ok); break;
-    }
-    return;
-  }
-  if (type == OP_DENSE1) {
-    T m[4];
+    case OP_DENSE1: {
+      T m[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      m[i].x = (R)op->m[2 * i];
-      m[i].y = (R)op->m[2 * i + 1];
+      for (int i = 0; i < 4; i++) {
+        m[i].x = (R)coef[o.coef + 2 * i];
+        m[i].y = (R)coef[o.coef + 2 * i + 1];
+      }
+      switch (o.t0) {
+        case 0: dense1<T, NE, 0, UNI>(v, m, em, ok); break;
+        case 1: if (RB > 1) dense1<T, NE, (RB > 1 ? 1 : 0), UNI>(v, m, em, ok); break;
+        case 2: if (RB > 2) dense1<T, NE, (RB > 2 ? 2 : 0), UNI>(v, m, em, ok); break;
+        case 3: if (RB > 3) dense1<T, NE, (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
+      }
+      break;
     }
-    switch (t0) {
-      case 0: dense1<T, NE, 0>(v, m, reg_mask, need, fixed_ok); break;
-      case 1: if (RB > 1) dense1<T, NE, (RB > 1 ? 1 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-      case 2: if (RB > 2) dense1<T, NE, (RB > 2 ? 2 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-      case 3: if (RB > 3) dense1<T, NE, (RB > 3 ? 3 : 0)>(v, m, reg_mask, need, fixed_ok); break;
+    case OP_PERM1:
+      switch (o.t0) {
+        case 0: perm1<T, NE, 0, UNI>(v, em, ok); break;
+        case 1: if (RB > 1) perm1<T, NE, (RB > 1 ? 1 : 0), UNI>(v, em, ok); break;
+        case 2: if (RB > 2) perm1<T, NE, (RB > 2 ? 2 : 0), UNI>(v, em, ok); break;
+        case 3: if (RB > 3) perm1<T, NE, (RB > 3 ? 3 : 0), UNI>(v, em, ok); break;
+      }
+      break;
+    default: {  // OP_DENSE2, t0 < t1
+      const double *m = coef + o.coef;
+      switch (o.t0 * 4 + o.t1) {
+        case 1: if (RB > 1) dense2<T, NE, 0, (RB > 1 ? 1 : 0), UNI>(v, m, em, ok); break;
+        case 2: if (RB > 2) dense2<T, NE, 0, (RB > 2 ? 2 : 0), UNI>(v, m, em, ok); break;
+        case 3: if (RB > 3) dense2<T, NE, 0, (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
+        case 6: if (RB > 2) dense2<T, NE, (RB > 2 ? 1 : 0), (RB > 2 ? 2 : 0), UNI>(v, m, em, ok); break;
+        case 7: if (RB > 3) dense2<T, NE, (RB > 3 ? 1 : 0), (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
+        case 11: if (RB > 3) dense2<T, NE, (RB > 3 ? 2 : 0), (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
+      }
     }
-    return;
-  }
-  // OP_DENSE2, t0 < t1
-  const int code = op->t0 * 4 + op->t1;
-  const double *m = op->m;
-  switch (code) {
-    case 1: if (RB > 1) dense2<T, NE, 0, (RB > 1 ? 1 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-    case 2: if (RB > 2) dense2<T, NE, 0, (RB > 2 ? 2 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-    case 3: if (RB > 3) dense2<T, NE, 0, (RB > 3 ? 3 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-    case 6: if (RB > 2) dense2<T, NE, (RB > 2 ? 1 : 0), (RB > 2 ? 2 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-    case 7: if (RB > 3) dense2<T, NE, (RB > 3 ? 1 : 0), (RB > 3 ? 3 : 0)>(v, m, reg_mask, need, fixed_ok); break;
-    case 11: if (RB > 3) dense2<T, NE, (RB > 3 ? 2 : 0), (RB > 3 ? 3 : 0)>(v, m, reg_mask, need, fixed_ok); break;
   }
 }
 
-template <typename R, int K, int RB>
+__host__ __device__ inline size_t shm_align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// dynamic shared memory layout of one launch (host and device agree)
+struct ShmSmem {
+  size_t ops, coef, phase, jtab, itoff, btab, total;
+};
+__host__ __device__ inline ShmSmem shm_smem_layout(int tile_bytes, int nbuf, int nops, int ncoef,
+                                                   int nphase, int nt, int ne) {
+  ShmSmem L;
+  size_t o = (size_t)tile_bytes * nbuf;
+  L.ops = o;
+  o = shm_align16(o + (size_t)nops * sizeof(ShmOp));
+  L.coef = o;
+  o = shm_align16(o + (size_t)ncoef * sizeof(double));
+  L.phase = o;
+  o = shm_align16(o + (size_t)nphase * sizeof(ShmPhase));
+  L.jtab = o;
+  o = shm_align16(o + (size_t)nphase * nt * sizeof(uint32_t));
+  L.itoff = o;
+  o = shm_align16(o + (size_t)ne * sizeof(uint64_t));
+  L.btab = o;
+  o = shm_align16(o + (size_t)4 * 256 * sizeof(uint64_t));
+  L.total = o;
+  return L;
+}
+
+// Persistent shared-memory kernel.  One CTA loops over tiles; with NBUF = 2
+// the next tile's HBM->SMEM copy (cp.async) overlaps the current tile's
+// register phases and store.  Everything that does not depend on the tile --
+// the op program, per-phase thread indices, per-iteration global offsets and
+// the tile-base deposit tables -- is staged in SMEM once per CTA.  The
+// swizzle is linear over GF(2), so shared addresses are XORs of per-thread
+// and per-element parts.
+template <typename R, int K, int RB, int NBUF>
 __global__ void __launch_bounds__(1 << (K - RB)) shm_kernel(
-    typename Cplx<R>::T *__restrict__ st, ShmLaunch sl, const uint64_t *__restrict__ hightab,
-    const ShmOp *__restrict__ ops, const ShmPhase *__restrict__ phases) {
+    typename Cplx<R>::T *__restrict__ st, ShmLaunch sl, const ShmOp *__restrict__ gops,
+    const double *__restrict__ gcoef, const ShmPhase *__restrict__ gph) {
   using T = typename Cplx<R>::T;
   constexpr int NT = 1 << (K - RB);
   constexpr int NE = 1 << RB;
   constexpr int TILE = 1 << K;
-  extern __shared__ unsigned char smraw[];
-  T *sm = reinterpret_cast<T *>(smraw);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const ShmSmem lay = shm_smem_layout(TILE * (int)sizeof(T), NBUF, sl.nops, sl.ncoef, sl.nphase, NT, NE);
+  T *buf = reinterpret_cast<T *>(smraw);
+  ShmOp *ops = reinterpret_cast<ShmOp *>(smraw + lay.ops);
+  double *coef = reinterpret_cast<double *>(smraw + lay.coef);
+  ShmPhase *ph = reinterpret_cast<ShmPhase *>(smraw + lay.phase);
+  uint32_t *jtab = reinterpret_cast<uint32_t *>(smraw + lay.jtab);  // (swz(jt) << 16) | jt
+  uint64_t *itoff = reinterpret_cast<uint64_t *>(smraw + lay.itoff);
+  uint64_t *btab = reinterpret_cast<uint64_t *>(smraw + lay.btab);
   const int tid = threadIdx.x;
-  const int c0 = sl.c0;
-  const int lowmask = (1 << c0) - 1;
-  const uint64_t *ht = hightab + sl.hightab_off;
-  const ShmOp *op0 = ops + sl.ops_off;
-  const ShmPhase *ph0 = phases + sl.phase_off;
 
-  for (uint64_t tile = blockIdx.x; tile < sl.ntiles; tile += gridDim.x) {
-    const uint64_t base = pdep64(tile, sl.nonactive);
-    // HBM -> SMEM: element j = it * NT + tid; consecutive threads read
-    // consecutive amplitudes inside runs of 2^c0 (c0 >= 5: 512 B for fp64).
+  // ---- stage the program and the index tables
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(gops + sl.ops_off);
+    uint4 *dst = reinterpret_cast<uint4 *>(ops);
+    for (int i = tid; i < sl.nops * 2; i += NT) dst[i] = src[i];
+    for (int i = tid; i < sl.ncoef; i += NT) coef[i] = gcoef[sl.coef_off + i];
+    for (int i = tid; i < sl.nphase; i += NT) ph[i] = gph[sl.phase_off + i];
+    // deposit tables of the tile base: base(tile) = OR_c btab[c][byte c of tile]
+    for (int i = tid; i < 4 * 256; i += NT) {
+      const int c = i >> 8;
+      uint64_t m = sl.nonactive;
+      for (int k = 0; k < 8 * c && m; k++) m &= m - 1;  // drop the lower 8c bits
+      btab[i] = pdep64((uint64_t)(i & 255), m);
+    }
+  }
+  __syncthreads();
+  for (int p = 0; p < sl.nphase; p++) {
+    int rmask = 0;
+#pragma unroll
+    for (int i = 0; i < RB; i++) rmask |= 1 << ph[p].rbit[i];
+    int jt = 0, t = tid;
+    for (int b = 0; b < K; b++) {
+      if ((rmask >> b) & 1) continue;
+      jt |= (t & 1) << b;
+      t >>= 1;
+    }
+    jtab[p * NT + tid] = ((uint32_t)swz<R>(jt) << 16) | (uint32_t)jt;
+  }
+  if (tid < NE) {
+    uint64_t o = 0;
+#pragma unroll
+    for (int i = 0; i < RB; i++)
+      if ((tid >> i) & 1) o |= 1ull << sl.act[K - RB + i];
+    itoff[tid] = o;
+  }
+  uint64_t off_t = 0;  // pdep(tid, lowest K-RB active slots)
+#pragma unroll
+  for (int i = 0; i < K - RB; i++)
+    if ((tid >> i) & 1) off_t |= 1ull << sl.act[i];
+  const int sw_tid = swz<R>(tid);
+  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);
+  __syncthreads();
+
+  auto tile_base = [&](uint64_t tile) {
+    return btab[tile & 255] | btab[256 + ((tile >> 8) & 255)] | btab[512 + ((tile >> 16) & 255)] |
+           btab[768 + ((tile >> 24) & 255)];
+  };
+  auto issue_load = [&](int bsel, uint64_t base) {
+    const T *g = st + base + off_t;
 #pragma unroll
     for (int it = 0; it < NE; it++) {
-      const int j = it * NT + tid;
-      const uint64_t off = (uint64_t)(j & lowmask) | ht[j >> c0];
-      cp_async(&sm[swz<R>(j)], &st[base + off]);
+      const unsigned sa = sm_base + (unsigned)((bsel * TILE + (sw_tid ^ swz<R>(it * NT))) * sizeof(T));
+      const T *ga = g + itoff[it];
+      if (sizeof(T) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(ga));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(ga));
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  uint64_t tile = blockIdx.x;
+  if (tile >= sl.ntiles) return;
+  uint64_t base = tile_base(tile);
+  issue_load(0, base);
+  int b = 0;
+  for (; tile < sl.ntiles; tile += gridDim.x) {
+    const uint64_t next = tile + gridDim.x;
+    uint64_t nbase = 0;
+    if (NBUF == 2 && next < sl.ntiles) {
+      nbase = tile_base(next);
+      issue_load(b ^ 1, nbase);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    T *tb = buf + b * TILE;
     for (int p = 0; p < sl.nphase; p++) {
-      const ShmPhase P = ph0[p];
-      int rmask = 0;
+      const ShmPhase P = ph[p];
+      const uint32_t jj = jtab[p * NT + tid];
+      const int jt = (int)(jj & 0xffffu), sj = (int)(jj >> 16);
+      int sr[RB];
 #pragma unroll
-      for (int i = 0; i < RB; i++) rmask |= 1 << P.rbit[i];
-      // thread part of the tile index: deposit tid into the non-register bits
-      int jt = 0;
-      {
-        int t = tid;
-        for (int b = 0; b < K; b++) {
-          if ((rmask >> b) & 1) continue;
-          jt |= (t & 1) << b;
-          t >>= 1;
-        }
-      }
-      int rv[RB];
+      for (int i = 0; i < RB; i++) sr[i] = swz<R>(1 << P.rbit[i]);
+      int ci[NE];
+      ci[0] = sj;
 #pragma unroll
-      for (int i = 0; i < RB; i++) rv[i] = 1 << P.rbit[i];
+      for (int e = 1; e < NE; e++) ci[e] = ci[e & (e - 1)] ^ sr[ctz_c(e)];
       T v[NE];
 #pragma unroll
-      for (int e = 0; e < NE; e++) {
-        int j = jt;
-#pragma unroll
-        for (int i = 0; i < RB; i++)
-          if ((e >> i) & 1) j |= rv[i];
-        v[e] = sm[swz<R>(j)];
+      for (int e = 0; e < NE; e++) v[e] = tb[ci[e]];
+      for (int oi = P.op_begin; oi < P.op_end; oi++) {
+        const ShmOp o = ops[oi];
+        if ((base & o.base_mask) != o.base_val) continue;  // tile-uniform
+        if (o.thr_mask == 0) {
+          apply_op<R, RB, true>(v, o, coef, true);
+        } else {
+          const bool ok = (jt & o.thr_mask) == o.thr_val;
+          if (!__any_sync(0xffffffffu, ok)) continue;
+          apply_op<R, RB, false>(v, o, coef, ok);
+        }
       }
-      for (int o = P.op_begin; o < P.op_end; o++) apply_op<R, RB>(v, op0 + o, jt, base);
 #pragma unroll
-      for (int e = 0; e < NE; e++) {
-        int j = jt;
-#pragma unroll
-        for (int i = 0; i < RB; i++)
-          if ((e >> i) & 1) j |= rv[i];
-        sm[swz<R>(j)] = v[e];
-      }
+      for (int e = 0; e < NE; e++) tb[ci[e]] = v[e];
       __syncthreads();
     }
-    // SMEM -> HBM, same coalesced pattern as the load
+    {
+      const T *tbc = tb;
+      T *g = st + base + off_t;
 #pragma unroll
-    for (int it = 0; it < NE; it++) {
-      const int j = it * NT + tid;
-      const uint64_t off = (uint64_t)(j & lowmask) | ht[j >> c0];
-      st[base + off] = sm[swz<R>(j)];
+      for (int it = 0; it < NE; it++) g[itoff[it]] = tbc[sw_tid ^ swz<R>(it * NT)];
     }
     __syncthreads();
+    if (NBUF == 1) {
+      if (next < sl.ntiles) {
+        nbase = tile_base(next);
+        issue_load(0, nbase);
+      }
+    } else {
+      b ^= 1;
+    }
+    base = nbase;
   }
-  (void)TILE;
 }
 
 // ---------------------------------------------------------- permute / misc
@@ -468,46 +544,57 @@ cudaError_t launch_fused(int dtype, void *st, int L, const FusedLaunch &fl, cons
                     : launch_fused_t<float>(st, L, fl, mats, s);
 }
 
-template <typename R, int K, int RB>
-static cudaError_t launch_shm_k(void *st, const ShmLaunch &sl, const uint64_t *ht,
-                                const ShmOp *ops, const ShmPhase *ph, cudaStream_t s) {
+template <typename R, int K, int RB, int NBUF>
+static cudaError_t launch_shm_k(void *st, const ShmLaunch &sl, const ShmOp *ops,
+                                const double *coef, const ShmPhase *ph, cudaStream_t s) {
   using T = typename Cplx<R>::T;
-  const size_t smem = sizeof(T) << K;
-  auto kern = shm_kernel<R, K, RB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  constexpr int NT = 1 << (K - RB);
+  const ShmSmem lay = shm_smem_layout((int)sizeof(T) << K, NBUF, sl.nops, sl.ncoef, sl.nphase,
+                                      NT, 1 << RB);
+  auto kern = shm_kernel<R, K, RB, NBUF>;
+  static int attr_set = 0;
+  if (attr_set < (int)lay.total) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.total);
+    if (e != cudaSuccess) return e;
+    attr_set = (int)lay.total;
   }
-  uint64_t grid = sl.ntiles;
-  const uint64_t cap = (uint64_t)1 << 30;
-  if (grid > cap) grid = cap;
-  kern<<<(unsigned)grid, 1 << (K - RB), smem, s>>>((T *)st, sl, ht, ops, ph);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, lay.total);
+  if (occ < 1) occ = 1;
+  uint64_t grid = (uint64_t)num_sms() * occ;
+  if (grid > sl.ntiles) grid = sl.ntiles;
+  kern<<<(unsigned)grid, NT, lay.total, s>>>((T *)st, sl, ops, coef, ph);
   return cudaGetLastError();
 }
 
+// tile configuration: (K, RB, NBUF).  Double buffering while two tiles fit.
 template <typename R>
-static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const uint64_t *ht,
-                                const ShmOp *ops, const ShmPhase *ph, cudaStream_t s) {
+static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const ShmOp *ops,
+                                const double *coef, const ShmPhase *ph, cudaStream_t s) {
+  constexpr bool F64 = sizeof(R) == 8;
   switch (sl.K) {
-    case 6: return launch_shm_k<R, 6, 1>(st, sl, ht, ops, ph, s);
-    case 7: return launch_shm_k<R, 7, 2>(st, sl, ht, ops, ph, s);
-    case 8: return launch_shm_k<R, 8, 3>(st, sl, ht, ops, ph, s);
-    case 9: return launch_shm_k<R, 9, 4>(st, sl, ht, ops, ph, s);
-    case 10: return launch_shm_k<R, 10, 4>(st, sl, ht, ops, ph, s);
-    case 11: return launch_shm_k<R, 11, 4>(st, sl, ht, ops, ph, s);
-    case 12: return launch_shm_k<R, 12, 4>(st, sl, ht, ops, ph, s);
-    case 13: return launch_shm_k<R, 13, 4>(st, sl, ht, ops, ph, s);
+    case 6: return launch_shm_k<R, 6, 1, 2>(st, sl, ops, coef, ph, s);
+    case 7: return launch_shm_k<R, 7, 2, 2>(st, sl, ops, coef, ph, s);
+    case 8: return launch_shm_k<R, 8, 3, 2>(st, sl, ops, coef, ph, s);
+    case 9: return launch_shm_k<R, 9, 4, 2>(st, sl, ops, coef, ph, s);
+    case 10: return launch_shm_k<R, 10, 4, 2>(st, sl, ops, coef, ph, s);
+    case 11: return sl.nbuf == 1 ? launch_shm_k<R, 11, 4, 1>(st, sl, ops, coef, ph, s)
+                                : launch_shm_k<R, 11, 4, 2>(st, sl, ops, coef, ph, s);
+    case 12: return sl.nbuf == 1 ? launch_shm_k<R, 12, 4, 1>(st, sl, ops, coef, ph, s)
+                                : launch_shm_k<R, 12, 4, 2>(st, sl, ops, coef, ph, s);
+    case 13: return F64 ? launch_shm_k<R, 13, 4, 1>(st, sl, ops, coef, ph, s)
+                        : launch_shm_k<R, 13, 4, 2>(st, sl, ops, coef, ph, s);
   }
   return cudaErrorInvalidValue;
 }
 
 int shm_register_bits(int K) { return K >= 9 ? 4 : K - 5; }
 
-cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const uint64_t *ht,
-                       const ShmOp *ops, const ShmPhase *ph, cudaStream_t s) {
-  return dtype == 0 ? launch_shm_t<double>(st, sl, ht, ops, ph, s)
-                    : launch_shm_t<float>(st, sl, ht, ops, ph, s);
+cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *ops,
+                       const double *coef, const ShmPhase *ph, cudaStream_t s) {
+  return dtype == 0 ? launch_shm_t<double>(st, sl, ops, coef, ph, s)
+                    : launch_shm_t<float>(st, sl, ops, coef, ph, s);
 }
 
 cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const int *newpos_host,

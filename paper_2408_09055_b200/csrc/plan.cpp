@@ -115,7 +115,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
   }
   C->nslots = (C->opt.virtual_world && C->world > 1) ? C->world : 1;
   C->prog.assign(C->nslots, {});
-  C->hightab.clear();
+  C->coef.clear();
   C->ops.clear();
   C->phases.clear();
   C->mats.clear();
@@ -395,39 +395,27 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           std::vector<int> act;
           for (int b = 0; b < L; b++)
             if ((amask >> b) & 1) act.push_back(b);
-          int c0 = 0;
-          while (c0 < K_ && act[c0] == c0) c0++;
           std::vector<int> tile_of_slot(L, -1);
           for (int b = 0; b < K_; b++) tile_of_slot[act[b]] = b;
+          ln.sl = ShmLaunch{};
           ln.sl.K = K_;
           ln.sl.RB = RB;
-          ln.sl.c0 = c0;
+          ln.sl.nbuf = (C->dt == ATLAS_C128 && K_ == 13) ? 1 : C->opt.shm_nbuf;
+          for (int b = 0; b < 16; b++) ln.sl.act[b] = b < K_ ? act[b] : 0;
           const u64 lmask = (L == 64) ? ~0ull : ((1ull << L) - 1);
           ln.sl.nonactive = lmask & ~amask;
           ln.sl.ntiles = 1ull << (L - K_);
-          ln.sl.hightab_off = (int64_t)C->hightab.size();
-          for (u64 h = 0; h < (1ull << (K_ - c0)); h++) {
-            u64 off = 0;
-            for (int b = c0; b < K_; b++)
-              if ((h >> (b - c0)) & 1) off |= 1ull << act[b];
-            C->hightab.push_back(off);
-          }
-          // ops (tile-bit targets first; register indices resolved per phase)
+          // ---- ops before register assignment
           struct Pre {
-            ShmOp op;
-            int ttile[2];
+            int type;
             int nt;
-            int sel_slot[3];
+            int ttile[2];
+            std::vector<std::pair<int, int>> sel;  // (physical slot, required value)
+            std::vector<double> coef;
           };
           std::vector<Pre> pre;
           if (!scalar_done) {
-            Pre p{};
-            p.op.type = OP_DIAG;
-            p.op.nsel = 0;
-            p.op.m[0] = scalar[sl].real();
-            p.op.m[1] = scalar[sl].imag();
-            p.nt = 0;
-            pre.push_back(p);
+            pre.push_back(Pre{OP_PHASE, 0, {0, 0}, {}, {scalar[sl].real(), scalar[sl].imag()}});
             scalar_done = true;
           }
           for (int gi : K.gates) {
@@ -438,13 +426,12 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               if (x.lrole[j] == TGT || x.lrole[j] == ANTI) tj[nt++] = j;
               else sj[ns++] = j;
             }
+            if (nt > 2) fail(ATLAS_E_UNSUPPORTED, "internal: gate with %d targets in shm kernel", nt);
             const int dl = 1 << x.nl;
             const int dt = 1 << nt;
             for (int sv = 0; sv < (1 << ns); sv++) {
-              // block for selector value sv
               cd blk[16];
               bool ident = true;
-              bool offsel = false;  // entries mixing selector values must vanish
               for (int r = 0; r < dt; r++)
                 for (int c = 0; c < dt; c++) {
                   int R = 0, Cc = 0;
@@ -459,44 +446,30 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                   blk[r * dt + c] = x.M[R * dl + Cc];
                   if (std::abs(blk[r * dt + c] - (r == c ? cd(1) : cd(0))) > 1e-15) ident = false;
                 }
-              (void)offsel;
-              if (nt == 0) {
-                // diagonal: collect all selector values into one DIAG op
-                if (sv == 0) {
-                  Pre p{};
-                  p.op.type = OP_DIAG;
-                  p.op.nsel = ns;
-                  p.nt = 0;
-                  for (int a = 0; a < ns; a++) p.sel_slot[a] = mp.sigma[x.lq[sj[a]]];
-                  pre.push_back(p);
-                }
-                pre.back().op.m[2 * sv] = blk[0].real();
-                pre.back().op.m[2 * sv + 1] = blk[0].imag();
-                continue;
-              }
               if (ident) continue;
-              Pre p{};
+              Pre p;
               p.nt = nt;
-              p.op.nsel = ns;
-              p.op.selv = sv;
-              for (int a = 0; a < ns; a++) p.sel_slot[a] = mp.sigma[x.lq[sj[a]]];
+              for (int a = 0; a < ns; a++) p.sel.push_back({mp.sigma[x.lq[sj[a]]], (sv >> a) & 1});
               for (int a = 0; a < nt; a++) {
                 int ts = tile_of_slot[mp.sigma[x.lq[tj[a]]]];
                 if (ts < 0) fail(ATLAS_E_INVALID, "internal: shm target not active");
                 p.ttile[a] = ts;
               }
-              if (nt == 1) {
+              if (nt == 0) {
+                p.type = OP_PHASE;
+                p.coef = {blk[0].real(), blk[0].imag()};
+              } else if (nt == 1) {
                 bool isx = std::abs(blk[0]) < 1e-15 && std::abs(blk[3]) < 1e-15 &&
                            std::abs(blk[1] - cd(1)) < 1e-15 && std::abs(blk[2] - cd(1)) < 1e-15;
-                p.op.type = isx ? OP_PERM1 : OP_DENSE1;
-                for (int i = 0; i < 4; i++) {
-                  p.op.m[2 * i] = blk[i].real();
-                  p.op.m[2 * i + 1] = blk[i].imag();
-                }
-              } else if (nt == 2) {
-                p.op.type = OP_DENSE2;
-                // canonical order: ttile[0] < ttile[1]
-                if (p.ttile[0] > p.ttile[1]) {
+                p.type = isx ? OP_PERM1 : OP_DENSE1;
+                if (!isx)
+                  for (int i = 0; i < 4; i++) {
+                    p.coef.push_back(blk[i].real());
+                    p.coef.push_back(blk[i].imag());
+                  }
+              } else {
+                p.type = OP_DENSE2;
+                if (p.ttile[0] > p.ttile[1]) {  // canonical order t0 < t1
                   std::swap(p.ttile[0], p.ttile[1]);
                   cd b2[16];
                   for (int r = 0; r < 4; r++)
@@ -507,17 +480,15 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                   std::copy(b2, b2 + 16, blk);
                 }
                 for (int i = 0; i < 16; i++) {
-                  p.op.m[2 * i] = blk[i].real();
-                  p.op.m[2 * i + 1] = blk[i].imag();
+                  p.coef.push_back(blk[i].real());
+                  p.coef.push_back(blk[i].imag());
                 }
-              } else {
-                fail(ATLAS_E_UNSUPPORTED, "internal: gate with %d targets in shm kernel", nt);
               }
               pre.push_back(p);
             }
           }
-          // register phases: greedy grouping by target tile bits (<= RB)
-          std::vector<std::pair<int, std::vector<int>>> groups;  // (mask, op indices)
+          // ---- register phases: greedy grouping by target tile bits (<= RB)
+          std::vector<std::pair<int, std::vector<int>>> groups;  // (target mask, op indices)
           for (int i = 0; i < (int)pre.size(); i++) {
             int tm = 0;
             for (int a = 0; a < pre[i].nt; a++) tm |= 1 << pre[i].ttile[a];
@@ -531,46 +502,57 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           if (groups.empty()) groups.push_back({0, {}});
           ln.sl.phase_off = (int64_t)C->phases.size();
           ln.sl.ops_off = (int64_t)C->ops.size();
+          ln.sl.coef_off = (int64_t)C->coef.size();
           ln.sl.nphase = (int)groups.size();
           for (auto &gr : groups) {
             int rm = gr.first;
-            // fill with the highest free tile bits (keeps low bits as lane bits)
+            // fill with the highest free tile bits (keeps low tile bits as lane bits)
             for (int b = K_ - 1; b >= 0 && popc((u64)rm) < RB; b--) rm |= 1 << b;
             ShmPhase ph{};
             int ri = 0;
             int reg_index[16];
-            for (int b = 0; b < K_; b++) {
-              reg_index[b] = -1;
+            for (int b = 0; b < 16; b++) reg_index[b] = -1;
+            for (int b = 0; b < K_; b++)
               if ((rm >> b) & 1) {
                 ph.rbit[ri] = b;
                 reg_index[b] = ri++;
               }
-            }
             for (int i = ri; i < 4; i++) ph.rbit[i] = 0;
             ph.op_begin = (int32_t)(C->ops.size() - ln.sl.ops_off);
             for (int i : gr.second) {
-              ShmOp op = pre[i].op;
-              if (pre[i].nt >= 1) op.t0 = reg_index[pre[i].ttile[0]];
-              if (pre[i].nt >= 2) op.t1 = reg_index[pre[i].ttile[1]];
-              for (int a = 0; a < op.nsel; a++) {
-                int slot = pre[i].sel_slot[a];
+              const Pre &p = pre[i];
+              ShmOp op{};
+              op.type = (uint8_t)p.type;
+              if (p.nt >= 1) op.t0 = (uint8_t)reg_index[p.ttile[0]];
+              if (p.nt >= 2) op.t1 = (uint8_t)reg_index[p.ttile[1]];
+              int reg_mask = 0, reg_val = 0;
+              for (auto &sv : p.sel) {
+                int slot = sv.first, v = sv.second;
                 int tb = tile_of_slot[slot];
                 if (tb < 0) {
-                  op.sel_src[a] = SEL_BASE;
-                  op.sel_idx[a] = slot;
+                  op.base_mask |= 1ull << slot;
+                  op.base_val |= (u64)v << slot;
                 } else if (reg_index[tb] >= 0) {
-                  op.sel_src[a] = SEL_REG;
-                  op.sel_idx[a] = reg_index[tb];
+                  reg_mask |= 1 << reg_index[tb];
+                  reg_val |= v << reg_index[tb];
                 } else {
-                  op.sel_src[a] = SEL_THR;
-                  op.sel_idx[a] = tb;
+                  op.thr_mask |= (uint16_t)(1 << tb);
+                  op.thr_val |= (uint16_t)(v << tb);
                 }
               }
+              // element mask over the 2^RB register elements (pair / quad bases
+              // for targeted ops: the target bits of e are zero there)
+              for (int e = 0; e < (1 << RB); e++)
+                if ((e & reg_mask) == reg_val) op.emask |= (uint16_t)(1u << e);
+              op.coef = (int32_t)(C->coef.size() - ln.sl.coef_off);
+              for (double d : p.coef) C->coef.push_back(d);
               C->ops.push_back(op);
             }
             ph.op_end = (int32_t)(C->ops.size() - ln.sl.ops_off);
             C->phases.push_back(ph);
           }
+          ln.sl.nops = (int)(C->ops.size() - ln.sl.ops_off);
+          ln.sl.ncoef = (int)(C->coef.size() - ln.sl.coef_off);
         }
         C->prog[sl].push_back(ln);
       }

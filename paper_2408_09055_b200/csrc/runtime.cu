@@ -22,8 +22,8 @@ void build_plan(atlas_ctx *C, int s_max, double cf);
 std::string plan_json(const atlas_ctx *C);
 cudaError_t launch_fused(int dtype, void *st, int L, const FusedLaunch &fl, const double2 *mats,
                          cudaStream_t s);
-cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const uint64_t *ht,
-                       const ShmOp *ops, const ShmPhase *ph, cudaStream_t s);
+cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *ops,
+                       const double *coef, const ShmPhase *ph, cudaStream_t s);
 cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const int *newpos_host,
                            const int *newpos_dev, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
@@ -137,7 +137,7 @@ static void upload(void *&d, const std::vector<T> &v) {
 
 static void ensure_blobs(atlas_ctx *C) {
   if (C->blobs_ready) return;
-  upload(C->d_hightab, C->hightab);
+  upload(C->d_coef, C->coef);
   upload(C->d_ops, C->ops);
   upload(C->d_phases, C->phases);
   upload(C->d_mats, C->mats);
@@ -284,7 +284,7 @@ void run(atlas_ctx *C) {
         switch (ln.type) {
           case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
           case L_SHM:
-            CK(launch_shm(dt, st, ln.sl, (const uint64_t *)C->d_hightab, (const ShmOp *)C->d_ops,
+            CK(launch_shm(dt, st, ln.sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                           (const ShmPhase *)C->d_phases, C->stream));
             break;
           case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;
@@ -399,7 +399,7 @@ void destroy(atlas_ctx *C) {
         if (C->d_state[s]) cudaFree(C->d_state[s]);
         if (C->d_scratch[s]) cudaFree(C->d_scratch[s]);
       }
-    for (void *p : {C->d_hightab, C->d_ops, C->d_phases, C->d_mats, C->d_newpos})
+    for (void *p : {C->d_coef, C->d_ops, C->d_phases, C->d_mats, C->d_newpos})
       if (p) cudaFree(p);
     for (auto e : C->ev) cudaEventDestroy(e);
     if (C->own_stream) cudaStreamDestroy(C->stream);
