@@ -1,0 +1,194 @@
+"""Host planner (C++ in libatlas_b200.so, through the C-ABI) against the
+oracle planners -- bit-exact where the oracle is exact (staging optimum with
+its canonical tie-break, OrderedKernelize), bounds + validity for Kernelize.
+CPU only: atlas_create/load/plan make no CUDA call."""
+import json
+import os
+
+import pytest
+
+from oracle import gates as OG, planner as P
+from workloads import circuits as C
+
+A = pytest.importorskip("paper_2408_09055_b200.atlas")
+try:
+    A.lib()
+except Exception as e:  # pragma: no cover
+    pytest.skip(f"library not built: {e}", allow_module_level=True)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_library_exports_every_header_symbol():
+    """include/atlas.h declares exactly the exported C entry points."""
+    import re
+    hdr = open(os.path.join(HERE, "..", "include", "atlas.h")).read()
+    declared = set(re.findall(r"\b(atlas_[a-z_0-9]+)\s*\(", hdr))
+    assert declared == set(A.SYMBOLS), declared ^ set(A.SYMBOLS)
+    lib = A.lib()
+    for s in declared:
+        assert hasattr(lib, s), s
+
+
+def test_errors_are_status_codes():
+    with pytest.raises(A.AtlasError) as e:
+        A.Simulator(10, world=3)
+    assert e.value.status == 1
+    s = A.Simulator(4)
+    with pytest.raises(A.AtlasError) as e:
+        s.load_circuit([C.Gate("CX", (0, 5))])
+    assert e.value.status == 1
+    with pytest.raises(A.AtlasError) as e:
+        s.run()  # before plan
+    assert e.value.status == 8
+    with pytest.raises(A.AtlasError) as e:
+        s.set_option("no_such_option", 1)
+    assert e.value.status == 2
+    # a gate with more non-insular qubits than L is infeasible
+    s = A.Simulator(3, world=4, virtual_world=1)
+    s.load_circuit([C.Gate("SWAP", (0, 1)), C.Gate("H", (2,))])
+    with pytest.raises(A.AtlasError) as e:
+        s.plan()
+    assert e.value.status == 3
+
+
+def product_plan(c, world, **opt):
+    s = A.Simulator(c.n, world=world, virtual_world=1 if world > 1 else 0, **opt)
+    s.load_circuit(c.gates)
+    s.plan(8, 3.0)
+    return s.plan_json()
+
+
+def masks(qs):
+    return sorted(qs)
+
+
+# ------------------------------------------------------------------ staging
+STAGING_CASES = [(C.ghz(3), 2), (C.qft(6), 8), (C.qft(5), 4), (C.ghz(6), 4)]
+STAGING_CASES += [(C.random_circuit(5, 9, 40 + s, kinds=("H", "X", "Z", "CX", "CZ", "CP", "RY", "T"),
+                                    max_arity=2), (2, 4, 8)[s % 3]) for s in range(10)]
+
+
+@pytest.mark.parametrize("case", range(len(STAGING_CASES)))
+def test_staging_matches_bruteforce(case):
+    """Minimum s (Thm. ilp-optimal), minimum objective (Eq. P:L1477)
+    and the canonical tie-break must equal the brute-force oracle bit for bit."""
+    c, world = STAGING_CASES[case]
+    G = world.bit_length() - 1
+    L = c.n - G
+    bf = P.stage_bruteforce(c, L=L, Gq=G, s_max=4, c=3)
+    pj = product_plan(c, world)
+    st = pj["staging"]
+    assert st["s"] == bf.s
+    assert st["cost"] == pytest.approx(bf.cost)
+    assert st["gate_stage"] == bf.gate_stage
+    for k in range(bf.s):
+        assert pj["stages"][k]["global"] == masks(bf.globals[k])
+        assert pj["stages"][k]["local"] == masks(bf.locals[k])
+
+
+def test_staging_c_invariance():
+    """With R = 0 the plan does not depend on c and J = (1 + c) * swaps
+    (reading R7; BASELINE config 5's c sweep)."""
+    c = C.qft(8)
+    plans = []
+    for cf in (1.0, 2.0, 3.0, 5.0, 10.0):
+        s = A.Simulator(8, world=4, virtual_world=1)
+        s.load_circuit(c.gates)
+        s.plan(8, cf)
+        pj = s.plan_json()
+        plans.append([st["global"] for st in pj["stages"]])
+        swaps = sum(len(set(pj["stages"][k]["global"]) - set(pj["stages"][k - 1]["global"]))
+                    for k in range(1, pj["staging"]["s"]))
+        assert pj["staging"]["cost"] == pytest.approx((1 + cf) * swaps)
+    assert all(p == plans[0] for p in plans)
+
+
+# ----------------------------------------------------------- kernelization
+def model_json(tmp_path, qmf=4, qms=6, ls=0, alpha=300, fus=(100, 110, 150, 400)):
+    d = {"fusion_cost": list(fus[:qmf]), "alpha": alpha,
+         "gate_cost": {k: {1: 20, 2: 30, 3: 40}[C.ARITY[k]] for k in C.KINDS},
+         "q_max_fusion": qmf, "q_max_shared": qms, "ls_qubits": ls}
+    p = tmp_path / "cm.json"
+    p.write_text(json.dumps(d))
+    return str(p), P.CostModel.from_json(d)
+
+
+def oracle_seq(c):
+    """Kernelizer input by the oracle's own insularity: active = operands that
+    are not diagonal-type (reading R16: anti-diagonal local qubits are active)."""
+    out = []
+    for g in c.gates:
+        ins = OG.insular_kind(g.kind, g.params)
+        out.append(P.KGate(frozenset(g.qubits),
+                           frozenset(q for q, t in zip(g.qubits, ins) if t != "diag"),
+                           g.kind))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_ordered_kernelize_matches_bruteforce(tmp_path, seed):
+    """OrderedKernelize == min over all contiguous segmentations,
+    with the same segments (canonical tie-break R7) and kinds."""
+    n = 7
+    c = C.random_circuit(n, 11, 600 + seed, kinds=("H", "X", "CX", "CZ", "CP", "RZ", "U3", "SWAP", "CCX"))
+    path, cm = model_json(tmp_path, ls=seed % 3)
+    pj = product_plan(c, 1, kernelizer=1, cost_model=path)
+    seq = oracle_seq(c)
+    ls = frozenset(range(seed % 3))
+    cost, segs = P.ordered_bruteforce(seq, cm, ls, n)
+    ks = pj["stages"][0]["kernels"]
+    assert pj["stages"][0]["kernel_cost"] == cost
+    assert [k["gates"] for k in ks] == [list(range(a, b)) for a, b, _ in segs]
+    assert [k["kind"] for k in ks] == [kd for _, _, kd in segs]
+
+
+@pytest.mark.parametrize("fam", ["qft", "ghz", "su2random", "ising", "qsvm", "wstate", "graphstate"])
+@pytest.mark.parametrize("lift", [0, 1])
+def test_kernelize_valid_and_not_worse_than_ordered(tmp_path, fam, lift):
+    """Thm. dp-correct: the kernels concatenate to a sequence
+    topologically equivalent to the stage; Thm. dp-optimal: cost
+    <= OrderedKernelize."""
+    n = 9
+    c = C.make(fam, n)
+    path, cm = model_json(tmp_path, qms=7, ls=2)
+    pj = product_plan(c, 1, kernelizer=0, cost_model=path, insular_lift=lift)
+    po = product_plan(c, 1, kernelizer=1, cost_model=path)
+    seq = oracle_seq(c)
+    ks = pj["stages"][0]["kernels"]
+    errs, cost = P.verify_plan([k["gates"] for k in ks], [k["kind"] for k in ks], seq, cm,
+                               frozenset(range(2)), n, lift=True, check_constraint1=False)
+    assert errs == []
+    assert cost == pj["stages"][0]["kernel_cost"]
+    assert cost <= po["stages"][0]["kernel_cost"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_kernelize_bounded_by_bruteforce(tmp_path, seed):
+    """BF_opt <= Kernelize (plain Constraint 1: no lifting, no attachment)."""
+    n = 5
+    c = C.random_circuit(n, 6, 800 + seed, kinds=("H", "CX", "CZ", "U3", "RZ"), max_arity=2)
+    path, cm = model_json(tmp_path, qms=6, qmf=4)
+    pj = product_plan(c, 1, kernelizer=0, cost_model=path, insular_lift=0, attach=0)
+    seq = oracle_seq(c)
+    bf, _ = P.kernel_bruteforce(seq, cm, frozenset(), n)
+    assert bf <= pj["stages"][0]["kernel_cost"]
+    ks = pj["stages"][0]["kernels"]
+    for k in ks:
+        assert P.satisfies_constraint1(set(k["gates"]), [g.qubits for g in seq])
+
+
+def test_kernelize_beats_ordered_on_su2random():
+    """The non-contiguous DP must find plans OrderedKernelize cannot
+    (App. P:L2390-2394, Fig. dp-pruning)."""
+    c = C.su2random(14)
+    pk = product_plan(c, 1, kernelizer=0, shm_qubits=8)
+    po = product_plan(c, 1, kernelizer=1, shm_qubits=8)
+    assert pk["stages"][0]["kernel_cost"] < 0.8 * po["stages"][0]["kernel_cost"]
+
+
+def test_greedy_baseline_is_fusion_up_to_5(tmp_path):
+    c = C.qft(10)
+    pj = product_plan(c, 1, kernelizer=2)
+    for k in pj["stages"][0]["kernels"]:
+        assert k["kind"] == "fusion" and len(k["qubits"]) <= 5
