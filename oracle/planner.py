@@ -28,7 +28,7 @@ Kernelization (PAPER.md §"Circuit Kernelization", App. P:L2348)
                         OrderedKernelize reaches, P:L2362 / Problem 1
                         P:L1639-1653); canonical tie-break = lexicographically
                         smallest tuple of segment starts read from the last
-                        segment backwards (reading R7), fusion preferred on a
+                        segment backwards (reading R21), fusion preferred on a
                         kind tie.
 ``satisfies_constraint1``  Constraint 1 by its quantifiers.
 ``extensible_qubits``   Def. "Extensible qubit" by its

@@ -69,7 +69,7 @@ static Kernel make_kernel(const std::vector<KGate> &seq, int a, int b, int kind,
 }
 
 // Alg. OrderedKernelize: DP[i+1] = min_j DP[j] + Cost(C[j..i]).
-// Ties keep the smallest j (R7).
+// Ties keep the smallest j (R21).
 KernelPlan ordered_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                              const KernelizeOptions &o) {
   const int m = (int)seq.size();

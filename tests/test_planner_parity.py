@@ -129,7 +129,7 @@ def oracle_seq(c):
 @pytest.mark.parametrize("seed", range(12))
 def test_ordered_kernelize_matches_bruteforce(tmp_path, seed):
     """OrderedKernelize == min over all contiguous segmentations,
-    with the same segments (canonical tie-break R7) and kinds."""
+    with the same segments (canonical tie-break R21) and kinds."""
     n = 7
     c = C.random_circuit(n, 11, 600 + seed, kinds=("H", "X", "CX", "CZ", "CP", "RZ", "U3", "SWAP", "CCX"))
     path, cm = model_json(tmp_path, ls=seed % 3)
