@@ -87,6 +87,8 @@ struct atlas_ctx {
   std::vector<double> coef;
   std::vector<atlas::ShmOp> ops;
   std::vector<atlas::ShmPhase> phases;
+  std::vector<atlas::DiagEnt> ents;
+  std::vector<atlas::PermTerm> terms;
   std::vector<double2> mats;
   std::vector<int> newpos;
 
@@ -99,7 +101,7 @@ struct atlas_ctx {
   std::vector<int> cur;                    // 0: state holds the data, 1: scratch
   bool bound = false;
   void *d_coef = nullptr, *d_ops = nullptr, *d_phases = nullptr, *d_mats = nullptr,
-       *d_newpos = nullptr;
+       *d_newpos = nullptr, *d_ents = nullptr, *d_terms = nullptr;
   std::vector<cudaEvent_t> ev;
   std::vector<float> launch_ms;
   std::vector<int> launch_kind;

@@ -100,6 +100,7 @@ struct Kernel {
   int kind = K_FUSION;
   u64 qubits = 0;          // logical qubits (fusion: all; shm: active + LSB)
   int64_t cost = 0;
+  int nphase = 0;          // shm: register phases of the lowered program (rank 0)
 };
 
 struct KernelPlan {

@@ -40,16 +40,9 @@ __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
   return r;
 }
 
-// Swizzle of a tile index so that the 8 (fp64) / 16 (fp32) lanes of one
-// shared-memory wavefront hit distinct 16-byte bank groups for the access
-// patterns of the load/store loops and of most register phases.
 template <typename R> __host__ __device__ constexpr int swz(int j);
-template <> __host__ __device__ constexpr int swz<double>(int j) {
-  return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7);
-}
-template <> __host__ __device__ constexpr int swz<float>(int j) {
-  return j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15);
-}
+template <> __host__ __device__ constexpr int swz<double>(int j) { return swz_c128(j); }
+template <> __host__ __device__ constexpr int swz<float>(int j) { return swz_c64(j); }
 
 template <typename T>
 __device__ __forceinline__ void cmac(T &acc, const T &a, const T &x) {
@@ -141,15 +134,16 @@ __global__ void __launch_bounds__(256) fused_kernel(typename Cplx<R>::T *__restr
 
 // ------------------------------------------------------------- shm kernel
 // Register-element loops are fully unrolled: e (and the pair partner) are
-// compile-time, the op's condition is a runtime bit mask over e.  UNI = the
-// op applies in every lane of the warp (no thread-bit selector).
-template <typename T, int NE, int TB, bool UNI>
+// compile-time.  CHK = the op is conditional: it applies where the runtime
+// element mask has bit e set and the thread predicate `ok` holds; unconditional
+// ops (OPF_FULL) compile to straight-line code.
+template <typename T, int NE, int TB, bool CHK>
 __device__ __forceinline__ void dense1(T (&v)[NE], const T (&m)[4], unsigned emask, bool ok) {
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     if (e & (1 << TB)) continue;
     const int e1 = e | (1 << TB);
-    if ((UNI || ok) && ((emask >> e) & 1u)) {
+    if (!CHK || (ok && ((emask >> e) & 1u))) {
       const T a = v[e], b = v[e1];
       T y0, y1;
       y0.x = m[0].x * a.x;
@@ -168,13 +162,13 @@ __device__ __forceinline__ void dense1(T (&v)[NE], const T (&m)[4], unsigned ema
   }
 }
 
-template <typename T, int NE, int TB, bool UNI>
+template <typename T, int NE, int TB, bool CHK>
 __device__ __forceinline__ void perm1(T (&v)[NE], unsigned emask, bool ok) {
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     if (e & (1 << TB)) continue;
     const int e1 = e | (1 << TB);
-    if ((UNI || ok) && ((emask >> e) & 1u)) {
+    if (!CHK || (ok && ((emask >> e) & 1u))) {
       const T a = v[e];
       v[e] = v[e1];
       v[e1] = a;
@@ -182,13 +176,13 @@ __device__ __forceinline__ void perm1(T (&v)[NE], unsigned emask, bool ok) {
   }
 }
 
-template <typename T, int NE, int TB0, int TB1, bool UNI>
+template <typename T, int NE, int TB0, int TB1, bool CHK>
 __device__ __forceinline__ void dense2(T (&v)[NE], const double *__restrict__ m, unsigned emask,
                                        bool ok) {
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     if (e & ((1 << TB0) | (1 << TB1))) continue;
-    if ((UNI || ok) && ((emask >> e) & 1u)) {
+    if (!CHK || (ok && ((emask >> e) & 1u))) {
       const int idx[4] = {e, e | (1 << TB0), e | (1 << TB1), e | (1 << TB0) | (1 << TB1)};
       T x[4], y[4];
 #pragma unroll
@@ -211,7 +205,15 @@ __device__ __forceinline__ void dense2(T (&v)[NE], const double *__restrict__ m,
   }
 }
 
-template <typename R, int RB, bool UNI>
+// multiply the elements selected by a factor slot (OP_DIAG) by f
+template <typename T, int NE, int SEL>
+__device__ __forceinline__ void diag_mul(T (&v)[NE], const T &f) {
+#pragma unroll
+  for (int e = 0; e < NE; e++)
+    if ((e & SEL) == SEL) v[e] = cmul(f, v[e]);
+}
+
+template <typename R, int RB, bool CHK>
 __device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB], const ShmOp &o,
                                          const double *__restrict__ coef, bool ok) {
   using T = typename Cplx<R>::T;
@@ -224,7 +226,7 @@ __device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB], cons
       c.y = (R)coef[o.coef + 1];
 #pragma unroll
       for (int e = 0; e < NE; e++)
-        if ((UNI || ok) && ((em >> e) & 1u)) v[e] = cmul(c, v[e]);
+        if (!CHK || (ok && ((em >> e) & 1u))) v[e] = cmul(c, v[e]);
       break;
     }
     case OP_DENSE1: {
@@ -235,32 +237,72 @@ __device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB], cons
         m[i].y = (R)coef[o.coef + 2 * i + 1];
       }
       switch (o.t0) {
-        case 0: dense1<T, NE, 0, UNI>(v, m, em, ok); break;
-        case 1: if (RB > 1) dense1<T, NE, (RB > 1 ? 1 : 0), UNI>(v, m, em, ok); break;
-        case 2: if (RB > 2) dense1<T, NE, (RB > 2 ? 2 : 0), UNI>(v, m, em, ok); break;
-        case 3: if (RB > 3) dense1<T, NE, (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
+        case 0: dense1<T, NE, 0, CHK>(v, m, em, ok); break;
+        case 1: if (RB > 1) dense1<T, NE, (RB > 1 ? 1 : 0), CHK>(v, m, em, ok); break;
+        case 2: if (RB > 2) dense1<T, NE, (RB > 2 ? 2 : 0), CHK>(v, m, em, ok); break;
+        case 3: if (RB > 3) dense1<T, NE, (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
       }
       break;
     }
     case OP_PERM1:
       switch (o.t0) {
-        case 0: perm1<T, NE, 0, UNI>(v, em, ok); break;
-        case 1: if (RB > 1) perm1<T, NE, (RB > 1 ? 1 : 0), UNI>(v, em, ok); break;
-        case 2: if (RB > 2) perm1<T, NE, (RB > 2 ? 2 : 0), UNI>(v, em, ok); break;
-        case 3: if (RB > 3) perm1<T, NE, (RB > 3 ? 3 : 0), UNI>(v, em, ok); break;
+        case 0: perm1<T, NE, 0, CHK>(v, em, ok); break;
+        case 1: if (RB > 1) perm1<T, NE, (RB > 1 ? 1 : 0), CHK>(v, em, ok); break;
+        case 2: if (RB > 2) perm1<T, NE, (RB > 2 ? 2 : 0), CHK>(v, em, ok); break;
+        case 3: if (RB > 3) perm1<T, NE, (RB > 3 ? 3 : 0), CHK>(v, em, ok); break;
       }
       break;
     default: {  // OP_DENSE2, t0 < t1
       const double *m = coef + o.coef;
       switch (o.t0 * 4 + o.t1) {
-        case 1: if (RB > 1) dense2<T, NE, 0, (RB > 1 ? 1 : 0), UNI>(v, m, em, ok); break;
-        case 2: if (RB > 2) dense2<T, NE, 0, (RB > 2 ? 2 : 0), UNI>(v, m, em, ok); break;
-        case 3: if (RB > 3) dense2<T, NE, 0, (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
-        case 6: if (RB > 2) dense2<T, NE, (RB > 2 ? 1 : 0), (RB > 2 ? 2 : 0), UNI>(v, m, em, ok); break;
-        case 7: if (RB > 3) dense2<T, NE, (RB > 3 ? 1 : 0), (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
-        case 11: if (RB > 3) dense2<T, NE, (RB > 3 ? 2 : 0), (RB > 3 ? 3 : 0), UNI>(v, m, em, ok); break;
+        case 1: if (RB > 1) dense2<T, NE, 0, (RB > 1 ? 1 : 0), CHK>(v, m, em, ok); break;
+        case 2: if (RB > 2) dense2<T, NE, 0, (RB > 2 ? 2 : 0), CHK>(v, m, em, ok); break;
+        case 3: if (RB > 3) dense2<T, NE, 0, (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
+        case 6: if (RB > 2) dense2<T, NE, (RB > 2 ? 1 : 0), (RB > 2 ? 2 : 0), CHK>(v, m, em, ok); break;
+        case 7: if (RB > 3) dense2<T, NE, (RB > 3 ? 1 : 0), (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
+        case 11: if (RB > 3) dense2<T, NE, (RB > 3 ? 2 : 0), (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
       }
     }
+  }
+}
+
+// OP_DIAG: accumulate the slot's factor (unconditional part times every
+// conditional entry whose thread/tile condition holds), then multiply it in.
+template <typename R, int RB>
+__device__ __forceinline__ void apply_diag(typename Cplx<R>::T (&v)[1 << RB], const ShmOp &o,
+                                           const double *__restrict__ coef,
+                                           const DiagEnt *__restrict__ ents, int jt,
+                                           uint64_t base) {
+  using T = typename Cplx<R>::T;
+  constexpr int NE = 1 << RB;
+  // the factor is accumulated in fp64 (a product of many unit phases)
+  double fx = coef[o.coef], fy = coef[o.coef + 1];
+  const int eb = (int)o.base_mask, ee = (int)o.base_val;
+  for (int i = eb; i < ee; i++) {
+    const DiagEnt &d = ents[i];
+    bool c = (jt & d.thr_mask) == d.thr_val;
+    if (d.has_base) c = c && ((base & d.base_mask) == d.base_val);
+    if (c) {
+      const double nx = fx * d.re - fy * d.im;
+      fy = fx * d.im + fy * d.re;
+      fx = nx;
+    }
+  }
+  T f;
+  f.x = (R)fx;
+  f.y = (R)fy;
+  switch (o.t0) {
+    case 0: diag_mul<T, NE, 0>(v, f); break;
+    case 1: diag_mul<T, NE, 1>(v, f); break;
+    case 2: if (RB > 1) diag_mul<T, NE, (RB > 1 ? 2 : 0)>(v, f); break;
+    case 3: if (RB > 2) diag_mul<T, NE, (RB > 2 ? 4 : 0)>(v, f); break;
+    case 4: if (RB > 3) diag_mul<T, NE, (RB > 3 ? 8 : 0)>(v, f); break;
+    case 5: if (RB > 1) diag_mul<T, NE, (RB > 1 ? 3 : 0)>(v, f); break;
+    case 6: if (RB > 2) diag_mul<T, NE, (RB > 2 ? 5 : 0)>(v, f); break;
+    case 7: if (RB > 3) diag_mul<T, NE, (RB > 3 ? 9 : 0)>(v, f); break;
+    case 8: if (RB > 2) diag_mul<T, NE, (RB > 2 ? 6 : 0)>(v, f); break;
+    case 9: if (RB > 3) diag_mul<T, NE, (RB > 3 ? 10 : 0)>(v, f); break;
+    case 10: if (RB > 3) diag_mul<T, NE, (RB > 3 ? 12 : 0)>(v, f); break;
   }
 }
 
@@ -268,20 +310,26 @@ __host__ __device__ inline size_t shm_align16(size_t x) { return (x + 15) & ~(si
 
 // dynamic shared memory layout of one launch (host and device agree)
 struct ShmSmem {
-  size_t ops, coef, phase, jtab, itoff, btab, total;
+  size_t ops, coef, phase, ents, terms, jtab, stab, itoff, btab, total;
 };
-__host__ __device__ inline ShmSmem shm_smem_layout(int tile_bytes, int nbuf, int nops, int ncoef,
-                                                   int nphase, int nt, int ne) {
+__host__ __device__ inline ShmSmem shm_smem_layout(int tile_bytes, int nbuf, const ShmLaunch &sl,
+                                                   int nt, int ne) {
   ShmSmem L;
   size_t o = (size_t)tile_bytes * nbuf;
   L.ops = o;
-  o = shm_align16(o + (size_t)nops * sizeof(ShmOp));
+  o = shm_align16(o + (size_t)sl.nops * sizeof(ShmOp));
   L.coef = o;
-  o = shm_align16(o + (size_t)ncoef * sizeof(double));
+  o = shm_align16(o + (size_t)sl.ncoef * sizeof(double));
   L.phase = o;
-  o = shm_align16(o + (size_t)nphase * sizeof(ShmPhase));
+  o = shm_align16(o + (size_t)sl.nphase * sizeof(ShmPhase));
+  L.ents = o;
+  o = shm_align16(o + (size_t)sl.nent * sizeof(DiagEnt));
+  L.terms = o;
+  o = shm_align16(o + (size_t)sl.nterm * sizeof(PermTerm));
   L.jtab = o;
-  o = shm_align16(o + (size_t)nphase * nt * sizeof(uint32_t));
+  o = shm_align16(o + (size_t)sl.nphase * nt * sizeof(uint32_t));
+  L.stab = o;
+  o = shm_align16(o + (size_t)sl.nphase * nt * sizeof(uint16_t));
   L.itoff = o;
   o = shm_align16(o + (size_t)ne * sizeof(uint64_t));
   L.btab = o;
@@ -293,25 +341,36 @@ __host__ __device__ inline ShmSmem shm_smem_layout(int tile_bytes, int nbuf, int
 // Persistent shared-memory kernel.  One CTA loops over tiles; with NBUF = 2
 // the next tile's HBM->SMEM copy (cp.async) overlaps the current tile's
 // register phases and store.  Everything that does not depend on the tile --
-// the op program, per-phase thread indices, per-iteration global offsets and
-// the tile-base deposit tables -- is staged in SMEM once per CTA.  The
-// swizzle is linear over GF(2), so shared addresses are XORs of per-thread
-// and per-element parts.
+// the op program, per-phase thread indices and store offsets, per-iteration
+// global offsets and the tile-base deposit tables -- is staged in SMEM once
+// per CTA.  The swizzle is linear over GF(2), so shared addresses are XORs of
+// per-thread and per-element parts; the same holds for the permuted store of
+// a phase whose affine permutation gates were folded into its addresses.
+// two CTAs per SM for the 256-thread configurations (register cap 128)
+template <typename R, int K, int RB>
+struct ShmMinBlocks {
+  static constexpr int value = ((K - RB) == 8 && (sizeof(R) << (K + 1)) <= 65536) ? 2 : 1;
+};
+
 template <typename R, int K, int RB, int NBUF>
-__global__ void __launch_bounds__(1 << (K - RB)) shm_kernel(
+__global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)) shm_kernel(
     typename Cplx<R>::T *__restrict__ st, ShmLaunch sl, const ShmOp *__restrict__ gops,
-    const double *__restrict__ gcoef, const ShmPhase *__restrict__ gph) {
+    const double *__restrict__ gcoef, const ShmPhase *__restrict__ gph,
+    const DiagEnt *__restrict__ gents, const PermTerm *__restrict__ gterms) {
   using T = typename Cplx<R>::T;
   constexpr int NT = 1 << (K - RB);
   constexpr int NE = 1 << RB;
   constexpr int TILE = 1 << K;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const ShmSmem lay = shm_smem_layout(TILE * (int)sizeof(T), NBUF, sl.nops, sl.ncoef, sl.nphase, NT, NE);
+  const ShmSmem lay = shm_smem_layout(TILE * (int)sizeof(T), NBUF, sl, NT, NE);
   T *buf = reinterpret_cast<T *>(smraw);
   ShmOp *ops = reinterpret_cast<ShmOp *>(smraw + lay.ops);
   double *coef = reinterpret_cast<double *>(smraw + lay.coef);
   ShmPhase *ph = reinterpret_cast<ShmPhase *>(smraw + lay.phase);
+  DiagEnt *ents = reinterpret_cast<DiagEnt *>(smraw + lay.ents);
+  PermTerm *terms = reinterpret_cast<PermTerm *>(smraw + lay.terms);
   uint32_t *jtab = reinterpret_cast<uint32_t *>(smraw + lay.jtab);  // (swz(jt) << 16) | jt
+  uint16_t *stab = reinterpret_cast<uint16_t *>(smraw + lay.stab);  // swz(A jt)
   uint64_t *itoff = reinterpret_cast<uint64_t *>(smraw + lay.itoff);
   uint64_t *btab = reinterpret_cast<uint64_t *>(smraw + lay.btab);
   const int tid = threadIdx.x;
@@ -323,6 +382,8 @@ __global__ void __launch_bounds__(1 << (K - RB)) shm_kernel(
     for (int i = tid; i < sl.nops * 2; i += NT) dst[i] = src[i];
     for (int i = tid; i < sl.ncoef; i += NT) coef[i] = gcoef[sl.coef_off + i];
     for (int i = tid; i < sl.nphase; i += NT) ph[i] = gph[sl.phase_off + i];
+    for (int i = tid; i < sl.nent; i += NT) ents[i] = gents[sl.ent_off + i];
+    for (int i = tid; i < sl.nterm; i += NT) terms[i] = gterms[sl.term_off + i];
     // deposit tables of the tile base: base(tile) = OR_c btab[c][byte c of tile]
     for (int i = tid; i < 4 * 256; i += NT) {
       const int c = i >> 8;
@@ -343,6 +404,11 @@ __global__ void __launch_bounds__(1 << (K - RB)) shm_kernel(
       t >>= 1;
     }
     jtab[p * NT + tid] = ((uint32_t)swz<R>(jt) << 16) | (uint32_t)jt;
+    uint32_t sa = 0;
+    if (ph[p].permuted)
+      for (int b = 0; b < K; b++)
+        if ((jt >> b) & 1) sa ^= ph[p].colimg[b];
+    stab[p * NT + tid] = (uint16_t)sa;
   }
   if (tid < NE) {
     uint64_t o = 0;
@@ -395,32 +461,53 @@ __global__ void __launch_bounds__(1 << (K - RB)) shm_kernel(
     __syncthreads();
     T *tb = buf + b * TILE;
     for (int p = 0; p < sl.nphase; p++) {
-      const ShmPhase P = ph[p];
+      const ShmPhase &P = ph[p];
       const uint32_t jj = jtab[p * NT + tid];
       const int jt = (int)(jj & 0xffffu), sj = (int)(jj >> 16);
       int sr[RB];
 #pragma unroll
       for (int i = 0; i < RB; i++) sr[i] = swz<R>(1 << P.rbit[i]);
-      int ci[NE];
-      ci[0] = sj;
-#pragma unroll
-      for (int e = 1; e < NE; e++) ci[e] = ci[e & (e - 1)] ^ sr[ctz_c(e)];
       T v[NE];
 #pragma unroll
-      for (int e = 0; e < NE; e++) v[e] = tb[ci[e]];
+      for (int e = 0; e < NE; e++) {
+        int a = sj;
+#pragma unroll
+        for (int i = 0; i < RB; i++)
+          if ((e >> i) & 1) a ^= sr[i];
+        v[e] = tb[a];
+      }
       for (int oi = P.op_begin; oi < P.op_end; oi++) {
-        const ShmOp o = ops[oi];
-        if ((base & o.base_mask) != o.base_val) continue;  // tile-uniform
-        if (o.thr_mask == 0) {
-          apply_op<R, RB, true>(v, o, coef, true);
+        const ShmOp &o = ops[oi];
+        if (o.type == OP_DIAG) {
+          apply_diag<R, RB>(v, o, coef, ents, jt, base);
+        } else if (o.flags & OPF_FULL) {
+          apply_op<R, RB, false>(v, o, coef, true);
         } else {
+          if ((base & o.base_mask) != o.base_val) continue;  // tile-uniform
           const bool ok = (jt & o.thr_mask) == o.thr_val;
           if (!__any_sync(0xffffffffu, ok)) continue;
-          apply_op<R, RB, false>(v, o, coef, ok);
+          apply_op<R, RB, true>(v, o, coef, ok);
         }
       }
+      int s0 = sj;
+      if (P.permuted) {
+        // folded affine permutation: value of tile index j -> A j ^ c(base)
+        uint32_t cb = P.c0_swz;
+        for (int i = P.term_begin; i < P.term_end; i++)
+          if ((base & terms[i].base_mask) == terms[i].base_val) cb ^= terms[i].vec_swz;
+        s0 = (int)(stab[p * NT + tid] ^ cb);
 #pragma unroll
-      for (int e = 0; e < NE; e++) tb[ci[e]] = v[e];
+        for (int i = 0; i < RB; i++) sr[i] = (int)P.colimg[P.rbit[i]];
+        __syncthreads();  // every thread has read its elements before any permuted store
+      }
+#pragma unroll
+      for (int e = 0; e < NE; e++) {
+        int a = s0;
+#pragma unroll
+        for (int i = 0; i < RB; i++)
+          if ((e >> i) & 1) a ^= sr[i];
+        tb[a] = v[e];
+      }
       __syncthreads();
     }
     {
@@ -546,11 +633,11 @@ cudaError_t launch_fused(int dtype, void *st, int L, const FusedLaunch &fl, cons
 
 template <typename R, int K, int RB, int NBUF>
 static cudaError_t launch_shm_k(void *st, const ShmLaunch &sl, const ShmOp *ops,
-                                const double *coef, const ShmPhase *ph, cudaStream_t s) {
+                                const double *coef, const ShmPhase *ph, const DiagEnt *ents,
+                                const PermTerm *terms, cudaStream_t s) {
   using T = typename Cplx<R>::T;
   constexpr int NT = 1 << (K - RB);
-  const ShmSmem lay = shm_smem_layout((int)sizeof(T) << K, NBUF, sl.nops, sl.ncoef, sl.nphase,
-                                      NT, 1 << RB);
+  const ShmSmem lay = shm_smem_layout((int)sizeof(T) << K, NBUF, sl, NT, 1 << RB);
   auto kern = shm_kernel<R, K, RB, NBUF>;
   static int attr_set = 0;
   if (attr_set < (int)lay.total) {
@@ -564,27 +651,28 @@ static cudaError_t launch_shm_k(void *st, const ShmLaunch &sl, const ShmOp *ops,
   if (occ < 1) occ = 1;
   uint64_t grid = (uint64_t)num_sms() * occ;
   if (grid > sl.ntiles) grid = sl.ntiles;
-  kern<<<(unsigned)grid, NT, lay.total, s>>>((T *)st, sl, ops, coef, ph);
+  kern<<<(unsigned)grid, NT, lay.total, s>>>((T *)st, sl, ops, coef, ph, ents, terms);
   return cudaGetLastError();
 }
 
 // tile configuration: (K, RB, NBUF).  Double buffering while two tiles fit.
 template <typename R>
 static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const ShmOp *ops,
-                                const double *coef, const ShmPhase *ph, cudaStream_t s) {
+                                const double *coef, const ShmPhase *ph, const DiagEnt *ents,
+                                const PermTerm *terms, cudaStream_t s) {
   constexpr bool F64 = sizeof(R) == 8;
   switch (sl.K) {
-    case 6: return launch_shm_k<R, 6, 1, 2>(st, sl, ops, coef, ph, s);
-    case 7: return launch_shm_k<R, 7, 2, 2>(st, sl, ops, coef, ph, s);
-    case 8: return launch_shm_k<R, 8, 3, 2>(st, sl, ops, coef, ph, s);
-    case 9: return launch_shm_k<R, 9, 4, 2>(st, sl, ops, coef, ph, s);
-    case 10: return launch_shm_k<R, 10, 4, 2>(st, sl, ops, coef, ph, s);
-    case 11: return sl.nbuf == 1 ? launch_shm_k<R, 11, 4, 1>(st, sl, ops, coef, ph, s)
-                                : launch_shm_k<R, 11, 4, 2>(st, sl, ops, coef, ph, s);
-    case 12: return sl.nbuf == 1 ? launch_shm_k<R, 12, 4, 1>(st, sl, ops, coef, ph, s)
-                                : launch_shm_k<R, 12, 4, 2>(st, sl, ops, coef, ph, s);
-    case 13: return F64 ? launch_shm_k<R, 13, 4, 1>(st, sl, ops, coef, ph, s)
-                        : launch_shm_k<R, 13, 4, 2>(st, sl, ops, coef, ph, s);
+    case 6: return launch_shm_k<R, 6, 1, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 7: return launch_shm_k<R, 7, 2, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 8: return launch_shm_k<R, 8, 3, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 9: return launch_shm_k<R, 9, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 10: return launch_shm_k<R, 10, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 11: return sl.nbuf == 1 ? launch_shm_k<R, 11, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
+                                : launch_shm_k<R, 11, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 12: return sl.nbuf == 1 ? launch_shm_k<R, 12, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
+                                : launch_shm_k<R, 12, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 13: return F64 ? launch_shm_k<R, 13, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
+                        : launch_shm_k<R, 13, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -592,9 +680,10 @@ static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const ShmOp *ops,
 int shm_register_bits(int K) { return K >= 9 ? 4 : K - 5; }
 
 cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *ops,
-                       const double *coef, const ShmPhase *ph, cudaStream_t s) {
-  return dtype == 0 ? launch_shm_t<double>(st, sl, ops, coef, ph, s)
-                    : launch_shm_t<float>(st, sl, ops, coef, ph, s);
+                       const double *coef, const ShmPhase *ph, const DiagEnt *ents,
+                       const PermTerm *terms, cudaStream_t s) {
+  return dtype == 0 ? launch_shm_t<double>(st, sl, ops, coef, ph, ents, terms, s)
+                    : launch_shm_t<float>(st, sl, ops, coef, ph, ents, terms, s);
 }
 
 cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const int *newpos_host,

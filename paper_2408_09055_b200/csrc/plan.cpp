@@ -20,7 +20,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <sstream>
+#include <tuple>
 
 #include "ctx.h"
 
@@ -56,6 +58,148 @@ int global_value(const StageMap &mp, int L, int rank, int q, const std::vector<i
   int slot = mp.sigma[q];
   return ((rank >> (slot - L)) & 1) ^ flip[q];
 }
+
+enum PreKind { PK_DIAG = 0, PK_AFF = 1, PK_DENSE = 2 };
+
+// one lowered block of a gate inside a shared-memory kernel
+struct Pre {
+  int type = OP_PHASE;
+  int nt = 0;
+  int ttile[2] = {0, 0};
+  std::vector<std::pair<int, int>> sel;  // (physical slot, required value)
+  std::vector<double> coef;
+  bool swap = false;  // OP_DENSE2 that is the SWAP permutation
+  int pk = PK_DENSE;
+  u32 tsel = 0;       // tile bits of the selectors
+  u32 tmask = 0;      // tile bits of the targets
+  // a diagonal op conjugated through the phase's folded permutations:
+  // c^(sum_k e_k * prod_{b in m_k} j_b) over monomials (m_k, e_k) of the
+  // register-phase tile index j (|m_k| <= 2), times the base selectors
+  bool conj = false;
+  std::vector<std::pair<u32, int>> mono;
+};
+
+// A register phase under construction.  items: (0, dense ops) or
+// (1, diagonal run), in execution order.  The affine map of the folded
+// permutation gates: tile index j -> A j ^ c(base), A given by its columns.
+struct PhaseB {
+  u32 R = 0;
+  std::vector<std::pair<int, std::vector<int>>> items;
+  bool diag_open = false;
+  u32 diag_bits = 0;
+  bool has_perm = false;
+  u32 PT = 0, PC = 0;  // tile bits targeted / used as controls by the folded gates
+  u32 col[16];
+  u32 c0 = 0;
+  std::vector<std::tuple<u64, u64, u32>> terms;  // (base_mask, base_val, vector)
+  PhaseB() {
+    for (int b = 0; b < 16; b++) col[b] = 1u << b;
+  }
+  // Express a diagonal op that follows the folded permutations in the tile
+  // index j the registers hold (D pi = pi D', D' = pi^-1 D pi): each tile
+  // selector (x_a == v) becomes (parity(j & row_a(A)) ^ c0_a == v).
+  // Supported: one selector with |row| <= 2, or two with |row| = 1.
+  bool conjugate(const Pre &p, const std::vector<int> &tile_of_slot, int K, Pre &out) const {
+    std::vector<std::pair<u32, int>> sels;  // (row mask, required parity)
+    for (auto &sv : p.sel) {
+      int a = tile_of_slot[sv.first];
+      if (a < 0) continue;
+      for (auto &t : terms)
+        if ((std::get<2>(t) >> a) & 1) return false;
+      u32 row = 0;
+      for (int b = 0; b < K; b++)
+        if ((col[b] >> a) & 1) row |= 1u << b;
+      sels.push_back({row, sv.second ^ (int)((c0 >> a) & 1)});
+    }
+    out = p;
+    out.conj = true;
+    out.mono.clear();
+    if (sels.size() == 1 && popc((u64)sels[0].first) <= 2) {
+      u32 r = sels[0].first;
+      int w = sels[0].second;
+      if (popc((u64)r) == 1) {
+        if (w) out.mono = {{r, 1}};
+        else out.mono = {{0u, 1}, {r, -1}};
+      } else {
+        u32 a = r & (~r + 1), b = r ^ a;
+        if (w) out.mono = {{a, 1}, {b, 1}, {r, -2}};
+        else out.mono = {{0u, 1}, {a, -1}, {b, -1}, {r, 2}};
+      }
+    } else if (sels.size() == 2 && popc((u64)sels[0].first) == 1 && popc((u64)sels[1].first) == 1 &&
+               sels[0].first != sels[1].first) {
+      u32 a = sels[0].first, b = sels[1].first;
+      int va = sels[0].second, vb = sels[1].second;
+      // [j_a == va][j_b == vb] expanded
+      if (va && vb) out.mono = {{a | b, 1}};
+      else if (va && !vb) out.mono = {{a, 1}, {a | b, -1}};
+      else if (!va && vb) out.mono = {{b, 1}, {a | b, -1}};
+      else out.mono = {{0u, 1}, {a, -1}, {b, -1}, {a | b, 1}};
+    } else {
+      return false;
+    }
+    out.tsel = 0;
+    for (auto &m : out.mono) out.tsel |= m.first;
+    return true;
+  }
+  // tile bits the net folded map moves or reads: a later op may run before
+  // the map only if its bits avoid these
+  u32 touched(int K) const {
+    u32 t = c0;
+    for (auto &tm : terms) t |= std::get<2>(tm);
+    for (int b = 0; b < K; b++)
+      if (col[b] != (1u << b)) t |= col[b] | (1u << b);
+    return t;
+  }
+  bool aff_identity(int K) const {
+    for (int b = 0; b < K; b++)
+      if (col[b] != (1u << b)) return false;
+    return c0 == 0 && terms.empty();
+  }
+  // compose x -> x ^ [x_c == v] e_t (CX), x -> x ^ e_t (X, optionally
+  // conditioned on tile-base bits), or the swap of tile bits a and b
+  void aff_apply(const Pre &p, const std::vector<int> &tile_of_slot, int K) {
+    has_perm = true;
+    auto lin_cx = [&](u32 x, int c, int t) { return ((x >> c) & 1) ? (x ^ (1u << t)) : x; };
+    auto lin_swap = [&](u32 x, int a, int b) {
+      u32 xa = (x >> a) & 1, xb = (x >> b) & 1;
+      if (xa != xb) x ^= (1u << a) | (1u << b);
+      return x;
+    };
+    if (p.type == OP_DENSE2) {  // SWAP
+      const int a = p.ttile[0], b = p.ttile[1];
+      for (int i = 0; i < K; i++) col[i] = lin_swap(col[i], a, b);
+      c0 = lin_swap(c0, a, b);
+      for (auto &t : terms) std::get<2>(t) = lin_swap(std::get<2>(t), a, b);
+      PT |= (1u << a) | (1u << b);
+      return;
+    }
+    const int t = p.ttile[0];
+    PT |= 1u << t;
+    int ctile = -1, cval = 1;
+    u64 bm = 0, bv = 0;
+    for (auto &sv : p.sel) {
+      int tb = tile_of_slot[sv.first];
+      if (tb >= 0) {
+        ctile = tb;
+        cval = sv.second;
+      } else {
+        bm |= 1ull << sv.first;
+        bv |= (u64)sv.second << sv.first;
+      }
+    }
+    if (ctile >= 0) {
+      PC |= 1u << ctile;
+      for (int i = 0; i < K; i++) col[i] = lin_cx(col[i], ctile, t);
+      c0 = lin_cx(c0, ctile, t);
+      if (!cval) c0 ^= 1u << t;
+      for (auto &tm : terms) std::get<2>(tm) = lin_cx(std::get<2>(tm), ctile, t);
+    } else if (bm == 0) {
+      c0 ^= 1u << t;
+    } else {
+      terms.push_back(std::make_tuple(bm, bv, 1u << t));
+    }
+  }
+};
 
 u64 ls_logical(const std::vector<int> &sigma, int ls) {
   u64 s = 0;
@@ -406,16 +550,12 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           ln.sl.nonactive = lmask & ~amask;
           ln.sl.ntiles = 1ull << (L - K_);
           // ---- ops before register assignment
-          struct Pre {
-            int type;
-            int nt;
-            int ttile[2];
-            std::vector<std::pair<int, int>> sel;  // (physical slot, required value)
-            std::vector<double> coef;
-          };
           std::vector<Pre> pre;
           if (!scalar_done) {
-            pre.push_back(Pre{OP_PHASE, 0, {0, 0}, {}, {scalar[sl].real(), scalar[sl].imag()}});
+            Pre p;
+            p.type = OP_PHASE;
+            p.coef = {scalar[sl].real(), scalar[sl].imag()};
+            pre.push_back(p);
             scalar_done = true;
           }
           for (int gi : K.gates) {
@@ -479,6 +619,12 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                     }
                   std::copy(b2, b2 + 16, blk);
                 }
+                bool isswap = true;
+                const int sw[4] = {0, 2, 1, 3};
+                for (int r = 0; r < 4; r++)
+                  for (int c = 0; c < 4; c++)
+                    if (std::abs(blk[r * 4 + c] - (c == sw[r] ? cd(1) : cd(0))) > 1e-15) isswap = false;
+                p.swap = isswap;
                 for (int i = 0; i < 16; i++) {
                   p.coef.push_back(blk[i].real());
                   p.coef.push_back(blk[i].imag());
@@ -487,25 +633,96 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               pre.push_back(p);
             }
           }
-          // ---- register phases: greedy grouping by target tile bits (<= RB)
-          std::vector<std::pair<int, std::vector<int>>> groups;  // (target mask, op indices)
-          for (int i = 0; i < (int)pre.size(); i++) {
-            int tm = 0;
-            for (int a = 0; a < pre[i].nt; a++) tm |= 1 << pre[i].ttile[a];
-            if (groups.empty() || popc((u64)(groups.back().first | tm)) > RB)
-              groups.push_back({tm, {i}});
-            else {
-              groups.back().first |= tm;
-              groups.back().second.push_back(i);
+          // ---- classify: diagonal / affine permutation (folded into the
+          // phase's store addresses) / dense (needs register residency)
+          for (Pre &p : pre) {
+            u32 tsel = 0;
+            int nts = 0, nbs = 0;
+            for (auto &sv : p.sel) {
+              int tb = tile_of_slot[sv.first];
+              if (tb >= 0) {
+                tsel |= 1u << tb;
+                nts++;
+              } else {
+                nbs++;
+              }
+            }
+            p.tsel = tsel;
+            if (p.type == OP_PHASE) p.pk = PK_DIAG;
+            else if (p.type == OP_PERM1 && (nts == 0 || (nts == 1 && nbs == 0))) p.pk = PK_AFF;
+            else if (p.type == OP_DENSE2 && p.swap && p.sel.empty()) p.pk = PK_AFF;
+            else p.pk = PK_DENSE;
+            p.tmask = 0;
+            for (int a = 0; a < p.nt; a++) p.tmask |= 1u << p.ttile[a];
+          }
+          // ---- register phases: dense ops need their target
+          // tile bits in registers (<= RB per phase); diagonal runs become
+          // factor slots; affine permutations are composed into the phase's
+          // store map.  Ops are only reordered across ops they commute with.
+          std::vector<PhaseB> phs(1);
+          const int npre = (int)pre.size();
+          for (int i = 0; i < npre; i++) {
+            const Pre p = pre[i];
+            PhaseB *cur = &phs.back();
+            auto fresh = [&]() {
+              phs.emplace_back();
+              cur = &phs.back();
+            };
+            if (p.pk == PK_AFF) {
+              cur->aff_apply(p, tile_of_slot, K_);
+              if (cur->aff_identity(K_)) cur->has_perm = false;  // e.g. CX RZ CX
+              continue;
+            }
+            if (p.pk == PK_DIAG) {
+              int idx = i;
+              if (cur->has_perm && (p.tsel & cur->touched(K_))) {
+                Pre q;
+                if (cur->conjugate(p, tile_of_slot, K_, q)) {
+                  pre.push_back(q);
+                  idx = (int)pre.size() - 1;
+                } else {
+                  fresh();
+                }
+              }
+              if (!cur->diag_open) {
+                cur->items.push_back({1, {}});
+                cur->diag_open = true;
+                cur->diag_bits = 0;
+              }
+              cur->items.back().second.push_back(idx);
+              cur->diag_bits |= pre[idx].tsel;
+              continue;
+            }
+            if (cur->has_perm && ((p.tmask | p.tsel) & cur->touched(K_))) fresh();
+            if (popc((u64)(cur->R | p.tmask)) > RB) fresh();
+            cur->R |= p.tmask;
+            if (cur->diag_open && !(p.tmask & cur->diag_bits)) {
+              // commutes with the open diagonal run: execute it first
+              const size_t n_it = cur->items.size();
+              if (n_it >= 2 && cur->items[n_it - 2].first == 0)
+                cur->items[n_it - 2].second.push_back(i);
+              else
+                cur->items.insert(cur->items.end() - 1, {0, {i}});
+            } else {
+              cur->diag_open = false;
+              if (!cur->items.empty() && cur->items.back().first == 0)
+                cur->items.back().second.push_back(i);
+              else
+                cur->items.push_back({0, {i}});
             }
           }
-          if (groups.empty()) groups.push_back({0, {}});
+          if (phs.size() > 1 && phs.back().items.empty() && !phs.back().has_perm) phs.pop_back();
           ln.sl.phase_off = (int64_t)C->phases.size();
           ln.sl.ops_off = (int64_t)C->ops.size();
           ln.sl.coef_off = (int64_t)C->coef.size();
-          ln.sl.nphase = (int)groups.size();
-          for (auto &gr : groups) {
-            int rm = gr.first;
+          ln.sl.ent_off = (int64_t)C->ents.size();
+          ln.sl.term_off = (int64_t)C->terms.size();
+          ln.sl.nphase = (int)phs.size();
+          auto swzh = [&](u32 j) -> u32 {
+            return (u32)(C->dt == ATLAS_C128 ? swz_c128((int)j) : swz_c64((int)j));
+          };
+          for (PhaseB &pb : phs) {
+            int rm = (int)pb.R;
             // fill with the highest free tile bits (keeps low tile bits as lane bits)
             for (int b = K_ - 1; b >= 0 && popc((u64)rm) < RB; b--) rm |= 1 << b;
             ShmPhase ph{};
@@ -519,13 +736,9 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               }
             for (int i = ri; i < 4; i++) ph.rbit[i] = 0;
             ph.op_begin = (int32_t)(C->ops.size() - ln.sl.ops_off);
-            for (int i : gr.second) {
-              const Pre &p = pre[i];
-              ShmOp op{};
-              op.type = (uint8_t)p.type;
-              if (p.nt >= 1) op.t0 = (uint8_t)reg_index[p.ttile[0]];
-              if (p.nt >= 2) op.t1 = (uint8_t)reg_index[p.ttile[1]];
-              int reg_mask = 0, reg_val = 0;
+            // selector split of one op: register / thread / tile-base parts
+            auto split = [&](const Pre &p, int &reg_mask, int &reg_val, ShmOp &op) {
+              reg_mask = reg_val = 0;
               for (auto &sv : p.sel) {
                 int slot = sv.first, v = sv.second;
                 int tb = tile_of_slot[slot];
@@ -540,19 +753,172 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                   op.thr_val |= (uint16_t)(v << tb);
                 }
               }
+            };
+            auto emit_generic = [&](const Pre &p) {
+              ShmOp op{};
+              op.type = (uint8_t)p.type;
+              if (p.nt >= 1) op.t0 = (uint8_t)reg_index[p.ttile[0]];
+              if (p.nt >= 2) op.t1 = (uint8_t)reg_index[p.ttile[1]];
+              int reg_mask, reg_val;
+              split(p, reg_mask, reg_val, op);
               // element mask over the 2^RB register elements (pair / quad bases
               // for targeted ops: the target bits of e are zero there)
               for (int e = 0; e < (1 << RB); e++)
                 if ((e & reg_mask) == reg_val) op.emask |= (uint16_t)(1u << e);
+              if (reg_mask == 0 && op.thr_mask == 0 && op.base_mask == 0) op.flags |= OPF_FULL;
               op.coef = (int32_t)(C->coef.size() - ln.sl.coef_off);
               for (double d : p.coef) C->coef.push_back(d);
               C->ops.push_back(op);
+            };
+            for (auto &item : pb.items) {
+              if (item.first == 0) {
+                for (int i : item.second) emit_generic(pre[i]);
+                continue;
+              }
+              // diagonal run -> factor slots.  A diagonal op multiplies by c
+              // where every selector holds; with register selectors (i, vi),
+              // (j, vj) the indicator [x_i = vi][x_j = vj] expands into
+              // products of F (1), K_i (x_i), K_j (x_j), P_ij (x_i x_j).
+              std::map<int, cd> uni;
+              std::map<int, std::map<std::tuple<uint16_t, uint16_t, u64, u64>, cd>> cond;
+              std::vector<int> generic;
+              auto pair_slot = [](int i, int j) {
+                static const int tab[4][4] = {{-1, 5, 6, 7}, {5, -1, 8, 9}, {6, 8, -1, 10}, {7, 9, 10, -1}};
+                return tab[i][j];
+              };
+              auto add = [&](int slot, const ShmOp &cnd, cd c) {
+                if (cnd.thr_mask == 0 && cnd.base_mask == 0) {
+                  auto it = uni.find(slot);
+                  if (it == uni.end()) uni[slot] = c;
+                  else it->second *= c;
+                } else {
+                  auto key = std::make_tuple(cnd.thr_mask, cnd.thr_val, cnd.base_mask, cnd.base_val);
+                  auto &m = cond[slot];
+                  auto it = m.find(key);
+                  if (it == m.end()) m[key] = c;
+                  else it->second *= c;
+                }
+              };
+              for (int i : item.second) {
+                const Pre &p = pre[i];
+                if (p.conj) {
+                  const cd c(p.coef[0], p.coef[1]);
+                  for (auto &mo : p.mono) {
+                    ShmOp cnd{};
+                    for (auto &sv : p.sel)
+                      if (tile_of_slot[sv.first] < 0) {
+                        cnd.base_mask |= 1ull << sv.first;
+                        cnd.base_val |= (u64)sv.second << sv.first;
+                      }
+                    int rr[2], nr = 0;
+                    for (int b = 0; b < K_; b++)
+                      if ((mo.first >> b) & 1) {
+                        if (reg_index[b] >= 0) rr[nr++] = reg_index[b];
+                        else {
+                          cnd.thr_mask |= (uint16_t)(1 << b);
+                          cnd.thr_val |= (uint16_t)(1 << b);
+                        }
+                      }
+                    const int slot = nr == 0 ? 0 : nr == 1 ? 1 + rr[0] : pair_slot(std::min(rr[0], rr[1]), std::max(rr[0], rr[1]));
+                    add(slot, cnd, std::pow(c, mo.second));
+                  }
+                  continue;
+                }
+                ShmOp tmp{};
+                int reg_mask, reg_val;
+                split(p, reg_mask, reg_val, tmp);
+                const int nreg = popc((u64)reg_mask);
+                if (nreg > 2) {
+                  generic.push_back(i);
+                  continue;
+                }
+                const cd c(p.coef[0], p.coef[1]), ci = cd(1) / c;
+                std::vector<std::pair<int, cd>> contrib;
+                int rb[2], rv[2], nr = 0;
+                for (int r = 0; r < RB; r++)
+                  if ((reg_mask >> r) & 1) {
+                    rb[nr] = r;
+                    rv[nr++] = (reg_val >> r) & 1;
+                  }
+                if (nr == 0) {
+                  contrib.push_back({0, c});
+                } else if (nr == 1) {
+                  if (rv[0]) contrib.push_back({1 + rb[0], c});
+                  else {
+                    contrib.push_back({0, c});
+                    contrib.push_back({1 + rb[0], ci});
+                  }
+                } else {
+                  const int ps = pair_slot(rb[0], rb[1]);
+                  if (rv[0] && rv[1]) {
+                    contrib.push_back({ps, c});
+                  } else if (rv[0] && !rv[1]) {
+                    contrib.push_back({1 + rb[0], c});
+                    contrib.push_back({ps, ci});
+                  } else if (!rv[0] && rv[1]) {
+                    contrib.push_back({1 + rb[1], c});
+                    contrib.push_back({ps, ci});
+                  } else {
+                    contrib.push_back({0, c});
+                    contrib.push_back({1 + rb[0], ci});
+                    contrib.push_back({1 + rb[1], ci});
+                    contrib.push_back({ps, c});
+                  }
+                }
+                for (auto &sc : contrib) add(sc.first, tmp, sc.second);
+              }
+              for (int slot = 0; slot < 11; slot++) {
+                auto iu = uni.find(slot);
+                auto ic = cond.find(slot);
+                cd u = iu == uni.end() ? cd(1) : iu->second;
+                bool has_c = ic != cond.end() && !ic->second.empty();
+                if (!has_c && std::abs(u - cd(1)) < 1e-15) continue;
+                ShmOp op{};
+                op.type = OP_DIAG;
+                op.t0 = (uint8_t)slot;
+                op.coef = (int32_t)(C->coef.size() - ln.sl.coef_off);
+                C->coef.push_back(u.real());
+                C->coef.push_back(u.imag());
+                op.base_mask = (u64)(C->ents.size() - ln.sl.ent_off);
+                if (has_c)
+                  for (auto &kv : ic->second) {
+                    DiagEnt d{};
+                    d.thr_mask = std::get<0>(kv.first);
+                    d.thr_val = std::get<1>(kv.first);
+                    d.base_mask = std::get<2>(kv.first);
+                    d.base_val = std::get<3>(kv.first);
+                    d.has_base = d.base_mask != 0;
+                    d.re = kv.second.real();
+                    d.im = kv.second.imag();
+                    C->ents.push_back(d);
+                  }
+                op.base_val = (u64)(C->ents.size() - ln.sl.ent_off);
+                C->ops.push_back(op);
+              }
+              for (int i : generic) emit_generic(pre[i]);
             }
             ph.op_end = (int32_t)(C->ops.size() - ln.sl.ops_off);
+            ph.term_begin = ph.term_end = (int32_t)(C->terms.size() - ln.sl.term_off);
+            if (pb.has_perm && !pb.aff_identity(K_)) {
+              ph.permuted = 1;
+              for (int b = 0; b < 16; b++) ph.colimg[b] = b < K_ ? (uint16_t)swzh(pb.col[b]) : 0;
+              ph.c0_swz = swzh(pb.c0);
+              for (auto &t : pb.terms) {
+                PermTerm pt{};
+                pt.base_mask = std::get<0>(t);
+                pt.base_val = std::get<1>(t);
+                pt.vec_swz = swzh(std::get<2>(t));
+                C->terms.push_back(pt);
+              }
+              ph.term_end = (int32_t)(C->terms.size() - ln.sl.term_off);
+            }
             C->phases.push_back(ph);
           }
+          if (sl == 0) C->kplans[k].kernels[&K - &kp.kernels[0]].nphase = (int)phs.size();
           ln.sl.nops = (int)(C->ops.size() - ln.sl.ops_off);
           ln.sl.ncoef = (int)(C->coef.size() - ln.sl.coef_off);
+          ln.sl.nent = (int)(C->ents.size() - ln.sl.ent_off);
+          ln.sl.nterm = (int)(C->terms.size() - ln.sl.term_off);
         }
         C->prog[sl].push_back(ln);
       }
@@ -610,6 +976,7 @@ std::string plan_json(const atlas_ctx *C) {
       const Kernel &K = C->kplans[k].kernels[i];
       if (i) o << ",";
       o << "{\"kind\":\"" << (K.kind == K_FUSION ? "fusion" : "shm") << "\",\"cost\":" << K.cost
+        << ",\"phases\":" << K.nphase
         << ",\"qubits\":";
       jmask(o, K.qubits);
       o << ",\"gates\":[";

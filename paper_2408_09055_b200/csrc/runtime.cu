@@ -23,7 +23,8 @@ std::string plan_json(const atlas_ctx *C);
 cudaError_t launch_fused(int dtype, void *st, int L, const FusedLaunch &fl, const double2 *mats,
                          cudaStream_t s);
 cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *ops,
-                       const double *coef, const ShmPhase *ph, cudaStream_t s);
+                       const double *coef, const ShmPhase *ph, const DiagEnt *ents,
+                       const PermTerm *terms, cudaStream_t s);
 cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const int *newpos_host,
                            const int *newpos_dev, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
@@ -142,6 +143,8 @@ static void ensure_blobs(atlas_ctx *C) {
   upload(C->d_phases, C->phases);
   upload(C->d_mats, C->mats);
   upload(C->d_newpos, C->newpos);
+  upload(C->d_ents, C->ents);
+  upload(C->d_terms, C->terms);
   C->blobs_ready = true;
 }
 
@@ -285,7 +288,8 @@ void run(atlas_ctx *C) {
           case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
           case L_SHM:
             CK(launch_shm(dt, st, ln.sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
-                          (const ShmPhase *)C->d_phases, C->stream));
+                          (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
+                          (const PermTerm *)C->d_terms, C->stream));
             break;
           case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;
           default: fail(ATLAS_E_INVALID, "internal: unexpected launch type %d", ln.type);
@@ -399,7 +403,7 @@ void destroy(atlas_ctx *C) {
         if (C->d_state[s]) cudaFree(C->d_state[s]);
         if (C->d_scratch[s]) cudaFree(C->d_scratch[s]);
       }
-    for (void *p : {C->d_coef, C->d_ops, C->d_phases, C->d_mats, C->d_newpos})
+    for (void *p : {C->d_coef, C->d_ops, C->d_phases, C->d_mats, C->d_newpos, C->d_ents, C->d_terms})
       if (p) cudaFree(p);
     for (auto e : C->ev) cudaEventDestroy(e);
     if (C->own_stream) cudaStreamDestroy(C->stream);

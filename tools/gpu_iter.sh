@@ -1,0 +1,14 @@
+#!/bin/bash
+# quick GPU iteration: parity tests + a few bench lines (no ncu)
+O=gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+tail -5 $O/pytest_gpu.log
+for w in ${WORKLOADS:-su2random_n28 qft_n28 ising_n28 qsvm_n28 ghz_n28}; do
+  timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --workload $w > $O/it_$w.json 2> $O/it_$w.err
+  python -c "
+import json
+d=json.loads(open('$O/it_$w.json').read().strip().splitlines()[-1])
+c=d['config']; r=d['roofline']
+print('$w', d['ms_per_step'], '%.3g'%d['value'], c['plan']['kernels'], c['kernel_ms_per_step'], r['kernel'], r['achieved'], r['frac'], r['avg_launch_ms'], d['clocks']['sm_mhz'])
+" || tail -3 $O/it_$w.err
+done
