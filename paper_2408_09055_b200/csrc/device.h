@@ -42,6 +42,7 @@ enum ShmOpType : uint8_t {
 // Op flags
 enum : uint8_t {
   OPF_FULL = 1,   // unconditional: every register element, every thread, every tile
+  OPF_REAL = 2,   // OP_DENSE1 whose 2x2 block is real (H, RY, ...): half the flops
 };
 
 // One op of a shared-memory kernel.  It acts on the register elements e with
@@ -84,7 +85,7 @@ static_assert(sizeof(DiagEnt) == 40, "DiagEnt layout");
 // colimg[b] = swz(A e_b) (the swizzle is linear, so addresses are XORs).
 struct PermTerm {
   uint64_t base_mask, base_val;
-  uint32_t vec_swz, pad;
+  uint32_t vec_swz, pad;       // swizzled tile vector
 };
 static_assert(sizeof(PermTerm) == 24, "PermTerm layout");
 

@@ -162,6 +162,26 @@ __device__ __forceinline__ void dense1(T (&v)[NE], const T (&m)[4], unsigned ema
   }
 }
 
+// real 2x2 block (m[i].y == 0): 8 flops per pair instead of 16
+template <typename T, int NE, int TB, bool CHK>
+__device__ __forceinline__ void dense1r(T (&v)[NE], const T (&m)[4], unsigned emask, bool ok) {
+#pragma unroll
+  for (int e = 0; e < NE; e++) {
+    if (e & (1 << TB)) continue;
+    const int e1 = e | (1 << TB);
+    if (!CHK || (ok && ((emask >> e) & 1u))) {
+      const T a = v[e], b = v[e1];
+      T y0, y1;
+      y0.x = fma(m[1].x, b.x, m[0].x * a.x);
+      y0.y = fma(m[1].x, b.y, m[0].x * a.y);
+      y1.x = fma(m[3].x, b.x, m[2].x * a.x);
+      y1.y = fma(m[3].x, b.y, m[2].x * a.y);
+      v[e] = y0;
+      v[e1] = y1;
+    }
+  }
+}
+
 template <typename T, int NE, int TB, bool CHK>
 __device__ __forceinline__ void perm1(T (&v)[NE], unsigned emask, bool ok) {
 #pragma unroll
@@ -236,11 +256,20 @@ __device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB], cons
         m[i].x = (R)coef[o.coef + 2 * i];
         m[i].y = (R)coef[o.coef + 2 * i + 1];
       }
-      switch (o.t0) {
-        case 0: dense1<T, NE, 0, CHK>(v, m, em, ok); break;
-        case 1: if (RB > 1) dense1<T, NE, (RB > 1 ? 1 : 0), CHK>(v, m, em, ok); break;
-        case 2: if (RB > 2) dense1<T, NE, (RB > 2 ? 2 : 0), CHK>(v, m, em, ok); break;
-        case 3: if (RB > 3) dense1<T, NE, (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
+      if (!CHK && (o.flags & OPF_REAL)) {
+        switch (o.t0) {
+          case 0: dense1r<T, NE, 0, CHK>(v, m, em, ok); break;
+          case 1: if (RB > 1) dense1r<T, NE, (RB > 1 ? 1 : 0), CHK>(v, m, em, ok); break;
+          case 2: if (RB > 2) dense1r<T, NE, (RB > 2 ? 2 : 0), CHK>(v, m, em, ok); break;
+          case 3: if (RB > 3) dense1r<T, NE, (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
+        }
+      } else {
+        switch (o.t0) {
+          case 0: dense1<T, NE, 0, CHK>(v, m, em, ok); break;
+          case 1: if (RB > 1) dense1<T, NE, (RB > 1 ? 1 : 0), CHK>(v, m, em, ok); break;
+          case 2: if (RB > 2) dense1<T, NE, (RB > 2 ? 2 : 0), CHK>(v, m, em, ok); break;
+          case 3: if (RB > 3) dense1<T, NE, (RB > 3 ? 3 : 0), CHK>(v, m, em, ok); break;
+        }
       }
       break;
     }
@@ -450,9 +479,8 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)
   int b = 0;
   for (; tile < sl.ntiles; tile += gridDim.x) {
     const uint64_t next = tile + gridDim.x;
-    uint64_t nbase = 0;
+    const uint64_t nbase = next < sl.ntiles ? tile_base(next) : 0;
     if (NBUF == 2 && next < sl.ntiles) {
-      nbase = tile_base(next);
       issue_load(b ^ 1, nbase);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
@@ -518,10 +546,7 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)
     }
     __syncthreads();
     if (NBUF == 1) {
-      if (next < sl.ntiles) {
-        nbase = tile_base(next);
-        issue_load(0, nbase);
-      }
+      if (next < sl.ntiles) issue_load(0, nbase);
     } else {
       b ^= 1;
     }
@@ -735,7 +760,7 @@ cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaS
 }
 
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s) {
-  const size_t bytes = (dtype == 0 ? 16 : 8) << L;
+  const size_t bytes = (dtype == 0 ? (size_t)16 : (size_t)8) << L;
   cudaError_t e = cudaMemsetAsync(st, 0, bytes, s);
   if (e != cudaSuccess || !one) return e;
   if (dtype == 0)

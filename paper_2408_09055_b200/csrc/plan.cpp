@@ -766,6 +766,12 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               for (int e = 0; e < (1 << RB); e++)
                 if ((e & reg_mask) == reg_val) op.emask |= (uint16_t)(1u << e);
               if (reg_mask == 0 && op.thr_mask == 0 && op.base_mask == 0) op.flags |= OPF_FULL;
+              if (p.type == OP_DENSE1) {
+                bool real = true;
+                for (int i = 0; i < 4; i++)
+                  if (p.coef[2 * i + 1] != 0.0) real = false;
+                if (real) op.flags |= OPF_REAL;
+              }
               op.coef = (int32_t)(C->coef.size() - ln.sl.coef_off);
               for (double d : p.coef) C->coef.push_back(d);
               C->ops.push_back(op);

@@ -120,3 +120,68 @@ def test_tile_sizes():
         psi, plan = run(c, shm_qubits=k)
         assert plan["K_tile"] == k
         check(psi, ref)
+
+
+# ---------------------------------------------------------------- full size
+# BASELINE config 2 sizes (n = 28, 4 GiB fp64 state) in the launch
+# configuration bench.py times, checked on sampled outputs that have closed
+# forms or by properties that hold at any size (P7).
+
+def _sample_idx(n, k=64, seed=0):
+    rng = np.random.default_rng(seed)
+    return sorted({0, (1 << n) - 1} | {int(x) for x in rng.integers(0, 1 << n, size=k)})
+
+
+def _amps(s, idx):
+    return np.array([s.get_state(i, 1)[0] for i in idx])
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_ghz_full_size_twice(dtype):
+    """ghz n=28: amplitudes 1/sqrt2 at 0 and 2^n-1, 0 elsewhere (P1).  Run
+    twice on one context: atlas_run must reset the state to |0...0>."""
+    n = 28
+    c = C.ghz(n)
+    md = TOL[dtype][0]
+    with A.Simulator(n, dtype, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        for _ in range(2):
+            s.run()
+            idx = _sample_idx(n)
+            got = _amps(s, idx)
+            want = np.array([2 ** -0.5 if i in (0, (1 << n) - 1) else 0.0 for i in idx])
+            assert np.abs(got - want).max() <= md
+
+
+def test_qft_full_size_basis_state():
+    """qft n=28 from a basis state |x>: amp(y) = 2^{-n/2} exp(2 pi i rev(x) y / 2^n) (P4)."""
+    n = 28
+    x = 0x5A3C1F7 & ((1 << n) - 1)
+    c = C.prepend_basis(C.qft(n), x)
+    rev = int(format(x, f"0{n}b")[::-1], 2)
+    with A.Simulator(n, 0, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.run()
+        idx = _sample_idx(n, 128, 1)
+        got = _amps(s, idx)
+    want = np.array([np.exp(2j * np.pi * ((rev * y) % (1 << n)) / (1 << n)) for y in idx]) * 2 ** (-n / 2)
+    assert np.abs(got - want).max() <= 1e-10
+
+
+@pytest.mark.parametrize("fam", ["su2random", "ising", "qsvm"])
+def test_mirror_full_size(fam):
+    """C followed by C^dagger returns |0...0> (P7), n = 28, the bench
+    workload family in the bench's kernelizer configuration."""
+    n = 28
+    c = C.mirror(C.make(fam, n))
+    with A.Simulator(n, 0, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.run()
+        a0 = s.get_state(0, 1)[0]
+        idx = _sample_idx(n, 32, 2)[1:]
+        rest = _amps(s, idx)
+    assert abs(a0 - 1) <= 1e-10
+    assert np.abs(rest).max() <= 1e-10
