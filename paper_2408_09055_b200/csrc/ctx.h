@@ -52,6 +52,9 @@ struct Options {
   int device = -1;
   long stage_budget = 2000000;
   int shm_nbuf = 1;
+  int shm_direct_store = 1;
+  int shm_rb = 4;
+  int shm_explicit_perm = 0;
   std::string cost_model;
 };
 

@@ -85,9 +85,10 @@ static_assert(sizeof(DiagEnt) == 40, "DiagEnt layout");
 // colimg[b] = swz(A e_b) (the swizzle is linear, so addresses are XORs).
 struct PermTerm {
   uint64_t base_mask, base_val;
+  uint64_t gvec;               // the vector deposited on the physical slots
   uint32_t vec_swz, pad;       // swizzled tile vector
 };
-static_assert(sizeof(PermTerm) == 24, "PermTerm layout");
+static_assert(sizeof(PermTerm) == 32, "PermTerm layout");
 
 struct ShmPhase {
   int32_t rbit[4];             // tile bits held in registers (RB used)
@@ -107,6 +108,14 @@ struct ShmLaunch {
   int64_t ops_off, coef_off, phase_off;
   int64_t ent_off, term_off;
   int32_t nent, nterm;
+  // last_direct: the last phase stores its registers straight to HBM (no
+  // shared-memory round trip); chosen when its register bits avoid the 5
+  // lowest tile bits, so the lanes of a warp cover contiguous 512-B runs.
+  // lcol[b] = physical offset of tile bit b under the last phase's folded
+  // map (1 << act[b] when it is the identity), lc0 = offset of its constant.
+  int32_t last_direct, pad;
+  uint64_t lcol[16];
+  uint64_t lc0;
 };
 
 // Fused dense kernel ("Fusion"): one 2^k x 2^k matrix on k slots.

@@ -376,13 +376,13 @@ __host__ __device__ inline ShmSmem shm_smem_layout(int tile_bytes, int nbuf, con
 // per-thread and per-element parts; the same holds for the permuted store of
 // a phase whose affine permutation gates were folded into its addresses.
 // two CTAs per SM for the 256-thread configurations (register cap 128)
-template <typename R, int K, int RB>
+template <typename R, int K, int RB, int NBUF>
 struct ShmMinBlocks {
-  static constexpr int value = ((K - RB) == 8 && (sizeof(R) << (K + 1)) <= 65536) ? 2 : 1;
+  static constexpr int value = (NBUF == 1 && (K - RB) >= 8 && (K - RB) <= 9 && (sizeof(R) << (K + 1)) <= 65536) ? 2 : 1;
 };
 
 template <typename R, int K, int RB, int NBUF>
-__global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)) shm_kernel(
+__global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB, NBUF>::value)) shm_kernel(
     typename Cplx<R>::T *__restrict__ st, ShmLaunch sl, const ShmOp *__restrict__ gops,
     const double *__restrict__ gcoef, const ShmPhase *__restrict__ gph,
     const DiagEnt *__restrict__ gents, const PermTerm *__restrict__ gterms) {
@@ -472,19 +472,38 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
+  const int last = sl.nphase - 1;
+  const bool ld = sl.last_direct != 0;
+  uint64_t gthr = 0;  // last phase, direct store: this thread's offset
+  __shared__ uint64_t limg[4];  // ... and the offsets of its register bits
+  if (ld) {
+    const int jtl = (int)(jtab[last * NT + tid] & 0xffffu);
+    for (int bb = 0; bb < K; bb++)
+      if ((jtl >> bb) & 1) gthr ^= sl.lcol[bb];
+    if (tid < RB) limg[tid] = sl.lcol[ph[last].rbit[tid]];
+    __syncthreads();
+  }
+  // ring of NBUF tile buffers: the loads of the next NBUF-1 tiles are in
+  // flight while a tile is processed (one cp.async group per tile; empty
+  // groups keep the group count uniform at the end of the range)
   uint64_t tile = blockIdx.x;
   if (tile >= sl.ntiles) return;
-  uint64_t base = tile_base(tile);
-  issue_load(0, base);
+  const uint64_t G = gridDim.x;
+#pragma unroll
+  for (int k = 0; k < NBUF - 1; k++) {
+    const uint64_t t = tile + (uint64_t)k * G;
+    if (t < sl.ntiles) issue_load(k, tile_base(t));
+    else asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   int b = 0;
-  for (; tile < sl.ntiles; tile += gridDim.x) {
-    const uint64_t next = tile + gridDim.x;
-    const uint64_t nbase = next < sl.ntiles ? tile_base(next) : 0;
-    if (NBUF == 2 && next < sl.ntiles) {
-      issue_load(b ^ 1, nbase);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  for (; tile < sl.ntiles; tile += G) {
+    const uint64_t base = tile_base(tile);
+    {
+      const uint64_t far = tile + (uint64_t)(NBUF - 1) * G;
+      const int fb = (b + NBUF - 1) % NBUF;  // freed at the end of the previous tile
+      if (far < sl.ntiles) issue_load(fb, tile_base(far));
+      else asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(NBUF - 1) : "memory");
     }
     __syncthreads();
     T *tb = buf + b * TILE;
@@ -517,6 +536,25 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)
           apply_op<R, RB, true>(v, o, coef, ok);
         }
       }
+      if (ld && p == last) {
+        // straight to HBM; a permuted map's images overlap, so offsets
+        // combine by XOR
+        uint64_t cg = gthr;
+        if (P.permuted) {
+          cg ^= sl.lc0;
+          for (int i = P.term_begin; i < P.term_end; i++)
+            if ((base & terms[i].base_mask) == terms[i].base_val) cg ^= terms[i].gvec;
+        }
+#pragma unroll
+        for (int e = 0; e < NE; e++) {
+          uint64_t o = cg;
+#pragma unroll
+          for (int i = 0; i < RB; i++)
+            if ((e >> i) & 1) o ^= limg[i];
+          st[base | o] = v[e];
+        }
+        break;
+      }
       int s0 = sj;
       if (P.permuted) {
         // folded affine permutation: value of tile index j -> A j ^ c(base)
@@ -538,19 +576,14 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB>::value)
       }
       __syncthreads();
     }
-    {
+    if (!ld) {
       const T *tbc = tb;
       T *g = st + base + off_t;
 #pragma unroll
       for (int it = 0; it < NE; it++) g[itoff[it]] = tbc[sw_tid ^ swz<R>(it * NT)];
     }
-    __syncthreads();
-    if (NBUF == 1) {
-      if (next < sl.ntiles) issue_load(0, nbase);
-    } else {
-      b ^= 1;
-    }
-    base = nbase;
+    __syncthreads();  // the buffer is free for the next load
+    b = (b + 1) % NBUF;
   }
 }
 
@@ -694,8 +727,14 @@ static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const ShmOp *ops,
     case 10: return launch_shm_k<R, 10, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
     case 11: return sl.nbuf == 1 ? launch_shm_k<R, 11, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
                                 : launch_shm_k<R, 11, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
-    case 12: return sl.nbuf == 1 ? launch_shm_k<R, 12, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
-                                : launch_shm_k<R, 12, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
+    case 12:
+      if (sl.RB == 3) return launch_shm_k<R, 12, 3, 1>(st, sl, ops, coef, ph, ents, terms, s);
+      // three tile buffers only while they fit the 227 KiB opt-in limit
+      if (sl.nbuf == 3 &&
+          shm_smem_layout((int)sizeof(typename Cplx<R>::T) << 12, 3, sl, 256, 16).total <= 232448)
+        return launch_shm_k<R, 12, 4, 3>(st, sl, ops, coef, ph, ents, terms, s);
+      return sl.nbuf == 1 ? launch_shm_k<R, 12, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
+                          : launch_shm_k<R, 12, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
     case 13: return F64 ? launch_shm_k<R, 13, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
                         : launch_shm_k<R, 13, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
   }

@@ -525,7 +525,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
         } else {
           ln.type = L_SHM;
           const int K_ = C->K_tile;
-          const int RB = shm_register_bits(K_);
+          const int RB = (K_ == 12 && C->opt.shm_rb == 3) ? 3 : shm_register_bits(K_);
           // active slots: kernel qubits (active set + LSB) padded to K_ slots
           u64 amask = 0;
           u64 qs = K.qubits;
@@ -668,7 +668,25 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               phs.emplace_back();
               cur = &phs.back();
             };
-            if (p.pk == PK_AFF) {
+            bool explicit_perm = false;
+            if (p.pk == PK_AFF && p.type == OP_PERM1 && C->opt.shm_explicit_perm &&
+                popc((u64)(cur->R | p.tmask)) <= RB) {
+              // Folding it would make a later dense op on its bits start a
+              // new phase; when such an op comes before the phase fills up,
+              // swap the registers explicitly instead (a few moves).
+              u32 rs = cur->R | p.tmask;
+              for (int q = i + 1; q < npre; q++) {
+                const Pre &pq = pre[q];
+                if (pq.pk != PK_DENSE) continue;
+                if (pq.tmask & (p.tmask | p.tsel)) {
+                  explicit_perm = true;
+                  break;
+                }
+                rs |= pq.tmask;
+                if (popc((u64)rs) > RB) break;
+              }
+            }
+            if (p.pk == PK_AFF && !explicit_perm) {
               cur->aff_apply(p, tile_of_slot, K_);
               if (cur->aff_identity(K_)) cur->has_perm = false;  // e.g. CX RZ CX
               continue;
@@ -914,6 +932,9 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                 pt.base_mask = std::get<0>(t);
                 pt.base_val = std::get<1>(t);
                 pt.vec_swz = swzh(std::get<2>(t));
+                u32 v = std::get<2>(t);
+                for (int b = 0; b < K_; b++)
+                  if ((v >> b) & 1) pt.gvec |= 1ull << act[b];
                 C->terms.push_back(pt);
               }
               ph.term_end = (int32_t)(C->terms.size() - ln.sl.term_off);
@@ -921,6 +942,26 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
             C->phases.push_back(ph);
           }
           if (sl == 0) C->kplans[k].kernels[&K - &kp.kernels[0]].nphase = (int)phs.size();
+          {
+            // direct HBM store of the last phase when its register bits
+            // avoid the 5 lowest tile bits (lanes = tile bits 0..4)
+            const ShmPhase &lp = C->phases.back();
+            const PhaseB &lb = phs.back();
+            int rm = 0;
+            for (int i = 0; i < RB; i++) rm |= 1 << lp.rbit[i];
+            const int lowm = (1 << std::min(5, K_ - RB)) - 1;
+            ln.sl.last_direct = C->opt.shm_direct_store && !(rm & lowm);
+            const bool perm = lp.permuted != 0;
+            auto dep = [&](u32 x) {
+              u64 r = 0;
+              for (int b = 0; b < K_; b++)
+                if ((x >> b) & 1) r |= 1ull << act[b];
+              return r;
+            };
+            for (int b = 0; b < 16; b++)
+              ln.sl.lcol[b] = b < K_ ? dep(perm ? lb.col[b] : (1u << b)) : 0;
+            ln.sl.lc0 = perm ? dep(lb.c0) : 0;
+          }
           ln.sl.nops = (int)(C->ops.size() - ln.sl.ops_off);
           ln.sl.ncoef = (int)(C->coef.size() - ln.sl.coef_off);
           ln.sl.nent = (int)(C->ents.size() - ln.sl.ent_off);

@@ -185,3 +185,16 @@ def test_mirror_full_size(fam):
         rest = _amps(s, idx)
     assert abs(a0 - 1) <= 1e-10
     assert np.abs(rest).max() <= 1e-10
+
+
+@pytest.mark.parametrize("opt", [
+    {"shm_direct_store": 0}, {"shm_explicit_perm": 1}, {"shm_rb": 3}, {"shm_nbuf": 2},
+    {"shm_nbuf": 3}, {"shm_direct_store": 0, "shm_explicit_perm": 1}])
+@pytest.mark.parametrize("fam", ["su2random", "qsvm", "random"])
+def test_shm_lowering_variants(fam, opt):
+    """Every shared-memory lowering variant (direct last-phase store, explicit
+    vs folded permutations, 3 or 4 register bits, 1-3 tile buffers) on a
+    13-qubit circuit, i.e. a 2^12 tile (K = 12) and a ragged 2-tile grid."""
+    c = C.random_circuit(13, 150, 77) if fam == "random" else C.make(fam, 13)
+    psi, _ = run(c, **opt)
+    check(psi, O.simulate(c))
