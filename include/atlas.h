@@ -212,6 +212,28 @@ atlas_status atlas_plan_stats(atlas_ctx *ctx, int64_t *out, int cap);
 atlas_status atlas_get_launches(atlas_ctx *ctx, float *ms, int32_t *kind,
                                 int64_t *bytes, int cap, int *count);
 
+/* One transfer of this rank's part of a remap exchange (the all-to-all of
+ * Alg. Execute's Shard): kind 0 = send `bytes` from
+ * src_off of the (packed) shard to `peer`; 1 = receive `bytes` from `peer`
+ * into dst_off of the new shard; 2 = local copy src_off -> dst_off (the
+ * 2^-g' share that stays on this rank).  Offsets are byte offsets into this
+ * rank's shard buffers. */
+typedef struct {
+  int32_t peer;
+  int32_t kind;
+  uint64_t src_off;
+  uint64_t dst_off;
+  uint64_t bytes;
+} atlas_xfer;
+
+/* The exchange schedule of the remap before stage `stage` (1 <= stage < s)
+ * for this context's rank -- exactly the transfers atlas_run issues (NCCL
+ * grouped send/recv, or device copies in virtual-world mode).  Host-only
+ * (needs a plan, no GPU).  Writes min(cap, total) records; *count = total
+ * (call with cap = 0 to size).  E_INVALID for a stage out of range. */
+atlas_status atlas_remap_schedule(atlas_ctx *ctx, int stage, atlas_xfer *out, int cap,
+                                  int *count);
+
 #ifdef __cplusplus
 }
 #endif

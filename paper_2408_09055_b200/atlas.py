@@ -32,7 +32,7 @@ SYMBOLS = [
     "atlas_create", "atlas_load_circuit", "atlas_plan", "atlas_run", "atlas_get_state",
     "atlas_set_state", "atlas_destroy", "atlas_last_error", "atlas_set_option_int",
     "atlas_set_option_str", "atlas_bind_buffers", "atlas_set_stream", "atlas_nccl_unique_id",
-    "atlas_get_plan_json", "atlas_plan_stats", "atlas_get_launches",
+    "atlas_get_plan_json", "atlas_plan_stats", "atlas_get_launches", "atlas_remap_schedule",
 ]
 
 
@@ -40,6 +40,15 @@ class AtlasError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class Xfer(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("src_off", ctypes.c_uint64), ("dst_off", ctypes.c_uint64),
+                ("bytes", ctypes.c_uint64)]
+
+
+XFER_KIND = {0: "send", 1: "recv", 2: "local"}
 
 
 class Gate(ctypes.Structure):
@@ -74,6 +83,7 @@ def lib():
             "atlas_get_plan_json": [vp, vp, sz, ctypes.POINTER(sz)],
             "atlas_plan_stats": [vp, vp, i32],
             "atlas_get_launches": [vp, vp, vp, vp, i32, ctypes.POINTER(i32)],
+            "atlas_remap_schedule": [vp, i32, vp, i32, ctypes.POINTER(i32)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -199,6 +209,16 @@ class Simulator:
                 "kernel_cost", "remaps", "plan_us", "staging_exact", "L", "G",
                 "launches_per_run"]
         return dict(zip(keys, list(v)))
+
+    def remap_schedule(self, stage: int):
+        """This rank's transfers of the remap before `stage`:
+        [(kind, peer, src_off, dst_off, bytes)] (host-only)."""
+        cnt = ctypes.c_int()
+        _check(lib().atlas_remap_schedule(self._ctx, stage, None, 0, ctypes.byref(cnt)))
+        buf = (Xfer * max(cnt.value, 1))()
+        _check(lib().atlas_remap_schedule(self._ctx, stage, buf, cnt.value, ctypes.byref(cnt)))
+        return [(XFER_KIND[x.kind], x.peer, x.src_off, x.dst_off, x.bytes)
+                for x in buf[:cnt.value]]
 
     def launches(self):
         cnt = ctypes.c_int()

@@ -14,6 +14,7 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count);
 void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count);
 void destroy(atlas_ctx *C);
 void nccl_unique_id(void *out);
+std::vector<Xfer> exchange_schedule(const atlas_ctx *C, int k, int r);
 }  // namespace atlas
 
 using namespace atlas;
@@ -128,6 +129,24 @@ atlas_status atlas_set_state(atlas_ctx *C, const void *host, uint64_t first, uin
   GUARD({
     need(C != nullptr && (host != nullptr || count == 0), ATLAS_E_INVALID, "NULL argument");
     set_state(C, host, first, count);
+  })
+}
+
+atlas_status atlas_remap_schedule(atlas_ctx *C, int stage, atlas_xfer *out, int cap, int *count) {
+  GUARD({
+    need(C != nullptr && count != nullptr, ATLAS_E_INVALID, "NULL argument");
+    need(C->planned, ATLAS_E_ORDER, "atlas_remap_schedule before atlas_plan");
+    need(stage >= 1 && stage < C->sp.s, ATLAS_E_INVALID, "stage out of range");
+    need(cap == 0 || out != nullptr, ATLAS_E_INVALID, "out is NULL");
+    std::vector<Xfer> v = exchange_schedule(C, stage, C->rank);
+    *count = (int)v.size();
+    for (int i = 0; i < (int)v.size() && i < cap; i++) {
+      out[i].peer = v[i].peer;
+      out[i].kind = v[i].kind;
+      out[i].src_off = v[i].src_off;
+      out[i].dst_off = v[i].dst_off;
+      out[i].bytes = v[i].bytes;
+    }
   })
 }
 

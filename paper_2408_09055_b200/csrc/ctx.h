@@ -31,6 +31,16 @@ struct Exchange {
   bool packed = false;          // a pack launch precedes (source = scratch)
 };
 
+// one transfer of a rank's part of a remap exchange
+enum XferKind { XFER_SEND = 0, XFER_RECV = 1, XFER_LOCAL = 2 };
+struct Xfer {
+  int peer;            // the other rank (this rank for XFER_LOCAL)
+  int kind;
+  uint64_t src_off;    // byte offset in the (packed) source shard (send, local)
+  uint64_t dst_off;    // byte offset in the destination shard (recv, local)
+  uint64_t bytes;
+};
+
 struct StageMap {
   std::vector<int> sigma;       // logical -> physical slot during the stage
   std::vector<int> flip_end;    // per logical qubit: flip bit at the end of the stage

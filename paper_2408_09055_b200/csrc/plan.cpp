@@ -1015,7 +1015,26 @@ std::string plan_json(const atlas_ctx *C) {
     jmask(o, C->sp.global[k]);
     o << ",\"sigma\":[";
     for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].sigma[q];
+    o << "],\"flip_begin\":[";
+    for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].flip_begin[q];
+    o << "],\"flip_end\":[";
+    for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].flip_end[q];
     o << "],\"packed\":" << (k > 0 && C->exch[k].packed ? "true" : "false");
+    o << ",\"pack_newpos\":";
+    {
+      int64_t off = -1;
+      if (!C->prog.empty())
+        for (const Launch &ln : C->prog[0])
+          if (ln.stage == k && ln.type == L_PACK) off = ln.newpos_off;
+      if (off < 0) {
+        o << "null";
+      } else {
+        o << "[";
+        for (int i = 0; i < C->L; i++) o << (i ? "," : "") << C->newpos[off + i];
+        o << "]";
+      }
+    }
+    o << ",\"remap_qubits\":" << (k > 0 ? C->exch[k].gp : 0);
     o << ",\"gates\":[";
     for (size_t i = 0; i < C->stage_gates[k].size(); i++) o << (i ? "," : "") << C->stage_gates[k][i];
     o << "],\"kernel_cost\":" << C->kplans[k].total << ",\"kernels\":[";

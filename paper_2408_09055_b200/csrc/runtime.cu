@@ -154,66 +154,90 @@ static void *other_buf(atlas_ctx *C, int s) { return C->cur[s] ? C->d_state[s] :
 // sizes of the simulated ranks' world (virtual mode: slot == rank)
 static int slot_rank(const atlas_ctx *C, int s) { return C->nslots > 1 ? s : C->rank; }
 
-// Exchange of stage k (after the optional pack) for all local slots.
-static void do_exchange(atlas_ctx *C, int k) {
+std::vector<Xfer> exchange_schedule(const atlas_ctx *C, int k, int r);
+
+// offset at which rank `to` receives the block `from` sends it
+static uint64_t recv_offset(const atlas_ctx *C, int k, int from, int to) {
+  for (const Xfer &x : exchange_schedule(C, k, to))
+    if (x.kind == XFER_RECV && x.peer == from) return x.dst_off;
+  fail(ATLAS_E_INVALID, "internal: no receive from %d at %d", from, to);
+  return 0;
+}
+
+// The exchange of the remap before stage k, for rank r (P:L1312 Shard;
+// SURVEY §8e): swapping the g' top local slots with the incoming qubits'
+// global slots splits the ranks into groups of 2^g' that differ only in the
+// swapped global bits; inside a group every rank sends block b (of 2^g'
+// contiguous blocks of its shard) to the rank whose swapped bits are b, where
+// it lands at block beta = (sender's swapped bits XOR their flips).
+std::vector<Xfer> exchange_schedule(const atlas_ctx *C, int k, int r) {
   const Exchange &ex = C->exch[k];
   const int gp = ex.gp;
-  const size_t blk = amp_bytes(C) << (C->L - gp);
+  const uint64_t blk = (uint64_t)amp_bytes(C) << (C->L - gp);
   const int nb = 1 << gp;
   u64 Gam = 0;
   for (int j = 0; j < gp; j++) Gam |= 1ull << ex.gamma[j];
-  auto dest = [&](int r, int b, int *rdst, int *beta) {
-    int rd = (int)(r & ~Gam);
+  auto dest = [&](int rr, int b, int *rdst, int *beta) {
+    int rd = (int)(rr & ~Gam);
     int bt = 0;
     for (int j = 0; j < gp; j++) {
       rd |= ((b >> j) & 1) << ex.gamma[j];
-      bt |= (((r >> ex.gamma[j]) & 1) ^ ex.fI[j]) << j;
+      bt |= (((rr >> ex.gamma[j]) & 1) ^ ex.fI[j]) << j;
     }
     *rdst = rd;
     *beta = bt;
   };
+  std::vector<Xfer> v;
+  if (gp == 0) return v;
+  for (int b = 0; b < nb; b++) {
+    int rd, bt;
+    dest(r, b, &rd, &bt);
+    if (rd == r) v.push_back(Xfer{r, XFER_LOCAL, (uint64_t)b * blk, (uint64_t)bt * blk, blk});
+    else v.push_back(Xfer{rd, XFER_SEND, (uint64_t)b * blk, 0, blk});
+  }
+  int myb = 0;  // the block every peer sends me = my swapped bits
+  for (int j = 0; j < gp; j++) myb |= ((r >> ex.gamma[j]) & 1) << j;
+  for (int pb = 0; pb < nb; pb++) {
+    int p = (int)(r & ~Gam);
+    for (int j = 0; j < gp; j++) p |= ((pb >> j) & 1) << ex.gamma[j];
+    if (p == r) continue;
+    int rd, bt;
+    dest(p, myb, &rd, &bt);
+    v.push_back(Xfer{p, XFER_RECV, 0, (uint64_t)bt * blk, blk});
+  }
+  return v;
+}
+
+// Exchange of stage k (after the optional pack) for all local slots.
+static void do_exchange(atlas_ctx *C, int k) {
+  if (C->exch[k].gp == 0) return;
   if (C->nslots > 1) {
-    // virtual world: all shards on this device
+    // virtual world: all shards on this device; sends become device copies
     for (int r = 0; r < C->nslots; r++) {
       const char *src = (const char *)cur_buf(C, r);
-      for (int b = 0; b < nb; b++) {
-        int rd, bt;
-        dest(r, b, &rd, &bt);
-        char *dst = (char *)other_buf(C, rd);
-        CK(cudaMemcpyAsync(dst + (size_t)bt * blk, src + (size_t)b * blk, blk,
-                           cudaMemcpyDeviceToDevice, C->stream));
+      for (const Xfer &x : exchange_schedule(C, k, r)) {
+        if (x.kind == XFER_RECV) continue;
+        char *dst = (char *)other_buf(C, x.peer);
+        const uint64_t doff = x.kind == XFER_LOCAL ? x.dst_off : recv_offset(C, k, x.peer, r);
+        CK(cudaMemcpyAsync(dst + doff, src + x.src_off, x.bytes, cudaMemcpyDeviceToDevice,
+                           C->stream));
       }
     }
     for (int r = 0; r < C->nslots; r++) C->cur[r] ^= 1;
     return;
   }
   if (C->world == 1) return;
-  const int r = C->rank;
   const char *src = (const char *)cur_buf(C, 0);
   char *dst = (char *)other_buf(C, 0);
-  // every peer p of my group sends me its block b = my bits at gamma; that
-  // block lands at beta(p) -- so I receive from p into dst + beta(p) * blk.
   NK(g_nccl.groupStart());
-  for (int b = 0; b < nb; b++) {
-    int rd, bt;
-    dest(r, b, &rd, &bt);
-    if (rd == r) {
-      CK(cudaMemcpyAsync(dst + (size_t)bt * blk, src + (size_t)b * blk, blk,
-                         cudaMemcpyDeviceToDevice, C->stream));
-      continue;
-    }
-    NK(g_nccl.send(src + (size_t)b * blk, blk, kNcclUint8, rd, C->nccl_comm, C->stream));
-  }
-  for (int pb = 0; pb < nb; pb++) {
-    // peer p: r with gamma bits replaced by pb
-    int p = (int)(r & ~Gam);
-    for (int j = 0; j < gp; j++) p |= ((pb >> j) & 1) << ex.gamma[j];
-    if (p == r) continue;
-    int myb = 0;  // the block index p sends me = my gamma bits
-    for (int j = 0; j < gp; j++) myb |= ((r >> ex.gamma[j]) & 1) << j;
-    int rd, bt;
-    dest(p, myb, &rd, &bt);
-    NK(g_nccl.recv(dst + (size_t)bt * blk, blk, kNcclUint8, p, C->nccl_comm, C->stream));
+  for (const Xfer &x : exchange_schedule(C, k, C->rank)) {
+    if (x.kind == XFER_LOCAL)
+      CK(cudaMemcpyAsync(dst + x.dst_off, src + x.src_off, x.bytes, cudaMemcpyDeviceToDevice,
+                         C->stream));
+    else if (x.kind == XFER_SEND)
+      NK(g_nccl.send(src + x.src_off, x.bytes, kNcclUint8, x.peer, C->nccl_comm, C->stream));
+    else
+      NK(g_nccl.recv(dst + x.dst_off, x.bytes, kNcclUint8, x.peer, C->nccl_comm, C->stream));
   }
   NK(g_nccl.groupEnd());
   C->cur[0] ^= 1;
