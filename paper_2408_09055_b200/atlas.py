@@ -185,6 +185,10 @@ class Simulator:
         """Copy into caller-owned host memory at address ptr (e.g. pinned)."""
         _check(lib().atlas_get_state(self._ctx, ptr, first, count))
 
+    def set_state_from(self, ptr: int, first: int, count: int):
+        """Copy from caller-owned host memory at address ptr (e.g. pinned)."""
+        _check(lib().atlas_set_state(self._ctx, ptr, first, count))
+
     def set_state(self, psi: np.ndarray, first: int = 0):
         a = np.ascontiguousarray(psi, dtype=self.np_dtype)
         _check(lib().atlas_set_state(self._ctx, a.ctypes.data, first, len(a)))

@@ -218,7 +218,7 @@ static void do_exchange(atlas_ctx *C, int k) {
       for (const Xfer &x : exchange_schedule(C, k, r)) {
         if (x.kind == XFER_RECV) continue;
         char *dst = (char *)other_buf(C, x.peer);
-        const uint64_t doff = x.kind == XFER_LOCAL ? x.dst_off : recv_offset(C, k, x.peer, r);
+        const uint64_t doff = x.kind == XFER_LOCAL ? x.dst_off : recv_offset(C, k, r, x.peer);
         CK(cudaMemcpyAsync(dst + doff, src + x.src_off, x.bytes, cudaMemcpyDeviceToDevice,
                            C->stream));
       }
@@ -371,10 +371,11 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
       uint64_t len = std::min<uint64_t>(end - x, (1ull << C->L) - off);
       int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
       if (s >= 0)
-        CK(cudaMemcpy((char *)host + (x - first) * B, (const char *)cur_buf(C, s) + off * B, len * B,
-                      cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync((char *)host + (x - first) * B, (const char *)cur_buf(C, s) + off * B,
+                           len * B, cudaMemcpyDeviceToHost, C->stream));
       x += len;
     }
+    CK(cudaStreamSynchronize(C->stream));
     return;
   }
   // general layout: bring the shard(s) to the host and gather
@@ -395,11 +396,29 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
 
 void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
   if (!C->planned) fail(ATLAS_E_ORDER, "atlas_set_state before atlas_plan");
-  if (first + count > (1ull << C->n)) fail(ATLAS_E_INVALID, "range out of bounds");
+  if (first + count > (1ull << C->n) || first + count < first) fail(ATLAS_E_INVALID, "range out of bounds");
   ensure_device(C);
+  CK(cudaSetDevice(C->device));
   const size_t B = amp_bytes(C);
   for (int s = 0; s < C->nslots; s++) C->cur[s] = 0;
-  // stage-0 layout has no flips
+  if (identity_layout(C, 0, false)) {
+    // logical == physical at stage 0: contiguous copies into each shard
+    uint64_t x = first, end = first + count;
+    while (x < end) {
+      int r = (int)(x >> C->L);
+      uint64_t off = x & ((1ull << C->L) - 1);
+      uint64_t len = std::min<uint64_t>(end - x, (1ull << C->L) - off);
+      int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
+      if (s >= 0)
+        CK(cudaMemcpyAsync((char *)C->d_state[s] + off * B, (const char *)host + (x - first) * B,
+                           len * B, cudaMemcpyHostToDevice, C->stream));
+      x += len;
+    }
+    CK(cudaStreamSynchronize(C->stream));
+    C->state_set = true;
+    return;
+  }
+  // general stage-0 layout: scatter on the host
   std::vector<std::vector<char>> sh(C->nslots);
   for (int s = 0; s < C->nslots; s++) {
     sh[s].resize(shard_bytes(C));
