@@ -164,7 +164,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     std::string k(key);
     Options &o = C->opt;
     bool replan = true;
-    if (k == "kernelizer") { need(v >= 0 && v <= 2, ATLAS_E_INVALID, "kernelizer in 0..2"); o.kernelizer = (int)v; }
+    if (k == "kernelizer") { need(v >= 0 && v <= 3, ATLAS_E_INVALID, "kernelizer in 0..3"); o.kernelizer = (int)v; }
     else if (k == "prune_T") o.prune_T = (int)v;
     else if (k == "ls_qubits") { need(v >= 0 && v <= 13, ATLAS_E_INVALID, "ls_qubits in 0..13"); o.ls_qubits = (int)v; }
     else if (k == "shm_qubits") o.shm_qubits = (int)v;
@@ -181,6 +181,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "stage_budget") o.stage_budget = (long)v;
     else if (k == "shm_direct_store") o.shm_direct_store = (int)v;
     else if (k == "shm_explicit_perm") o.shm_explicit_perm = (int)v;
+    else if (k == "front") o.front = (int)v;
     else if (k == "shm_rb") { need(v == 3 || v == 4, ATLAS_E_INVALID, "shm_rb is 3 or 4"); o.shm_rb = (int)v; }
     else if (k == "shm_nbuf") { need(v >= 1 && v <= 3, ATLAS_E_INVALID, "shm_nbuf is 1, 2 or 3"); o.shm_nbuf = (int)v; }
     else fail(ATLAS_E_UNSUPPORTED, "unknown option '%s'", key);

@@ -65,6 +65,7 @@ struct Options {
   int shm_direct_store = 1;
   int shm_rb = 4;
   int shm_explicit_perm = 0;
+  int front = 1;
   std::string cost_model;
 };
 

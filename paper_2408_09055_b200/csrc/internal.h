@@ -114,6 +114,7 @@ struct KernelizeOptions {
   bool lift = true;
   bool attach = true;
   int kinds = 3;
+  bool front = true;       // also consider the front packing (R29)
   int L = 0;               // local qubits (caps kernel sizes)
   u64 ls_set = 0;          // logical qubits at the forced LSB physical slots
 };
@@ -125,6 +126,8 @@ KernelPlan ordered_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                              const KernelizeOptions &o);
 KernelPlan greedy_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                             const KernelizeOptions &o);
+KernelPlan front_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
+                           const KernelizeOptions &o);
 KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                         const KernelizeOptions &o);
 // cost of a kernel made of these gates, best kind (fusion preferred on a tie)

@@ -138,3 +138,86 @@ KernelPlan greedy_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
 }
 
 }  // namespace atlas
+
+namespace atlas {
+
+// Commutation-aware greedy packing ("front" kernelizer).  Gates a < b must
+// keep their order iff they share a qubit that is non-diagonal in either
+// (the exact relation Thm. dp-correct's topological equivalence is checked
+// with).  Kernels are built one at a time from the ready front of
+// that dependency DAG: a ready gate joins the open kernel while the kernel
+// still fits (shared-memory: active set incl. the forced LSB qubits <=
+// q_max_shared; fusion-only: qubits <= q_max_fusion), the gate adding the
+// fewest new qubits first (ties: circuit order); gates made ready by it may
+// join the same kernel.  This finds column-wise packings of entangling
+// blocks (e.g. su2random's all-to-all CX blocks: one kernel per window of
+// target qubits across all rows) that the DP's deferred-merging heuristics
+// miss; Kernelize returns the cheapest valid candidate (R29).
+KernelPlan front_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
+                           const KernelizeOptions &o) {
+  const int m = (int)seq.size();
+  const Caps c = caps(cm, o);
+  const bool shm = c.qms >= 0;
+  const int cap = shm ? c.qms : c.qmf;
+  KernelPlan kp;
+  if (m == 0) return kp;
+  std::vector<std::vector<int>> succ(m);
+  std::vector<int> indeg(m, 0);
+  for (int a = 0; a < m; a++)
+    for (int b = a + 1; b < m; b++) {
+      const u64 sh = seq[a].qubits & seq[b].qubits;
+      if (sh && (sh & (seq[a].active | seq[b].active))) {
+        succ[a].push_back(b);
+        indeg[b]++;
+      }
+    }
+  std::vector<int> ready;
+  for (int g = 0; g < m; g++)
+    if (!indeg[g]) ready.push_back(g);
+  int done = 0;
+  while (done < m) {
+    Kernel K;
+    u64 q = 0, act = o.ls_set;
+    int64_t gs = 0;
+    for (;;) {
+      int best = -1, best_grow = 1 << 30, best_pos = -1;
+      for (int r = 0; r < (int)ready.size(); r++) {
+        const int g = ready[r];
+        const u64 nq = q | seq[g].qubits, na = act | seq[g].active;
+        const int size = shm ? popc(na) : popc(nq);
+        if (size > cap) continue;
+        const int grow = size - (shm ? popc(act) : popc(q));
+        if (grow < best_grow || (grow == best_grow && g < best)) {
+          best = g;
+          best_grow = grow;
+          best_pos = r;
+        }
+      }
+      if (best < 0) {
+        if (!K.gates.empty()) break;
+        // nothing fits an empty kernel of this kind: take the earliest ready gate alone
+        best_pos = 0;
+        for (int r = 1; r < (int)ready.size(); r++)
+          if (ready[r] < ready[best_pos]) best_pos = r;
+        best = ready[best_pos];
+      }
+      ready.erase(ready.begin() + best_pos);
+      K.gates.push_back(best);
+      q |= seq[best].qubits;
+      act |= seq[best].active;
+      gs += cm.gate_cost[seq[best].kind];
+      done++;
+      for (int s2 : succ[best])
+        if (--indeg[s2] == 0) ready.push_back(s2);
+    }
+    int kind = 0;
+    K.cost = cost_of(q, act, gs, cm, c, &kind);
+    K.kind = kind;
+    K.qubits = kind == K_FUSION ? q : act;
+    kp.total += K.cost;
+    kp.kernels.push_back(K);
+  }
+  return kp;
+}
+
+}  // namespace atlas

@@ -722,9 +722,18 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
             nu, (long long)kp.total, kp.kernels.size(), (long long)ordered.total,
             ordered.kernels.size(), (int)valid, C.arena.size());
   if (getenv("ATLAS_DEBUG_KEEP")) return kp;
-  if (!valid) return ordered;  // Thm. dp-correct violated: never expected
-  if (kp.total > ordered.total) return ordered;      // pruning made it worse
-  return kp;
+  // the cheapest valid candidate: the DP, OrderedKernelize (Thm. dp-optimal
+  // guarantees DP <= Ordered without pruning; pruning may worsen
+  // it) and the commutation-aware front packing (R29)
+  KernelPlan best_plan = ordered;
+  if (valid && kp.total <= best_plan.total) best_plan = kp;
+  if (o.front) {
+    KernelPlan fr = front_kernelize(seq, cm, o);
+    std::vector<int> ford;
+    for (auto &K : fr.kernels) ford.insert(ford.end(), K.gates.begin(), K.gates.end());
+    if (order_is_valid(seq, ford) && fr.total < best_plan.total) best_plan = fr;
+  }
+  return best_plan;
 }
 
 }  // namespace atlas

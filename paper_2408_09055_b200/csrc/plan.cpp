@@ -442,12 +442,14 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
     ko.lift = C->opt.lift != 0;
     ko.attach = C->opt.attach != 0;
     ko.kinds = C->opt.kinds;
+    ko.front = C->opt.front != 0;
     ko.L = L;
     ko.ls_set = ls_logical(mp.sigma, std::min(C->cm.ls_qubits, L));
     KernelPlan kp;
     if (!seq.empty()) {
       if (ko.algo == 1) kp = ordered_kernelize(seq, C->cm, ko);
       else if (ko.algo == 2) kp = greedy_kernelize(seq, C->cm, ko);
+      else if (ko.algo == 3) kp = front_kernelize(seq, C->cm, ko);
       else kp = dp_kernelize(seq, C->cm, ko);
     }
     // kernel gate indices are positions in seq; keep them for lowering and
