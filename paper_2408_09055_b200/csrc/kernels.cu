@@ -525,9 +525,12 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB, NBUF>::
       }
       for (int oi = P.op_begin; oi < P.op_end; oi++) {
         const ShmOp &o = ops[oi];
-        if (o.type == OP_DIAG) {
+        // one 16-byte shared load for the op header (type, t0, t1, flags, ...)
+        const uint4 hdr = *reinterpret_cast<const uint4 *>(&o);
+        const unsigned otype = hdr.x & 0xffu, oflags = (hdr.x >> 24) & 0xffu;
+        if (otype == OP_DIAG) {
           apply_diag<R, RB>(v, o, coef, ents, jt, base);
-        } else if (o.flags & OPF_FULL) {
+        } else if (oflags & OPF_FULL) {
           apply_op<R, RB, false>(v, o, coef, true);
         } else {
           if ((base & o.base_mask) != o.base_val) continue;  // tile-uniform

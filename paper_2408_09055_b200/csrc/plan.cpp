@@ -926,6 +926,24 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
             ph.op_end = (int32_t)(C->ops.size() - ln.sl.ops_off);
             ph.term_begin = ph.term_end = (int32_t)(C->terms.size() - ln.sl.term_off);
             if (pb.has_perm && !pb.aff_identity(K_)) {
+              // merge the tile-base terms: [b = 0] v = v ^ [b = 1] v, and terms
+              // with equal conditions XOR together (<= one per non-active bit
+              // for CX chains controlled by non-active qubits)
+              {
+                std::map<std::pair<u64, u64>, u32> mt;
+                for (auto &t : pb.terms) {
+                  u64 bm = std::get<0>(t), bv = std::get<1>(t);
+                  u32 v = std::get<2>(t);
+                  if (popc(bm) == 1 && bv == 0) {
+                    pb.c0 ^= v;
+                    bv = bm;
+                  }
+                  mt[{bm, bv}] ^= v;
+                }
+                pb.terms.clear();
+                for (auto &kv : mt)
+                  if (kv.second) pb.terms.push_back(std::make_tuple(kv.first.first, kv.first.second, kv.second));
+              }
               ph.permuted = 1;
               for (int b = 0; b < 16; b++) ph.colimg[b] = b < K_ ? (uint16_t)swzh(pb.col[b]) : 0;
               ph.c0_swz = swzh(pb.c0);
