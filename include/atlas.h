@@ -152,9 +152,15 @@ const char *atlas_last_error(void);
 
 /* ------------------------------------------------------------- options */
 /* Integer options (defaults in brackets):
- *   "kernelizer"     0 = Kernelize DP [0], 1 = OrderedKernelize
- *                    (P:L2354), 2 = greedy fusion packing up to 5 qubits
- *                    (the paper's baseline)
+ *   "kernelizer"     0 = Kernelize [0]: the cheapest valid of the
+ *                    DP, OrderedKernelize and the front packing (DESIGN.md
+ *                    R29); 1 = OrderedKernelize; 2 = greedy fusion
+ *                    packing up to 5 qubits (the paper's baseline);
+ *                    3 = front packing alone
+ *   "front"          consider the front packing inside Kernelize [1]
+ *   "dp_budget"      Kernelize DP state budget; beyond it the DP is abandoned
+ *                    for the cheaper of the other candidates [1000000];
+ *                    <= 0: no budget.  Deterministic (same on every rank).
  *   "prune_T"        Kernelize pruning threshold T [500];
  *                    <= 0 means no pruning
  *   "ls_qubits"      least-significant physical qubits forced into every
@@ -167,6 +173,11 @@ const char *atlas_last_error(void);
  *   "virtual_world"  1 = all ranks on this GPU (see atlas_create) [0]
  *   "init"           1 = atlas_run starts from |0...0> [1]
  *   "timing"         1 = per-launch CUDA events (atlas_get_launches) [0]
+ *   "shm_nbuf"       shared-memory tile buffers per CTA, 1..3 [1]
+ *   "shm_rb"         register bits per phase for 2^12 tiles, 3 or 4 [4]
+ *   "shm_direct_store"  last phase stores straight to HBM when coalesced [1]
+ *   "shm_explicit_perm" execute permutation gates in registers when a
+ *                    later dense op needs their bits (else folded) [0]
  *   "device"         CUDA device ordinal [current device]
  *   "stage_budget"   staging search state budget [2000000]
  * String options:

@@ -66,6 +66,7 @@ struct Options {
   int shm_rb = 4;
   int shm_explicit_perm = 0;
   int front = 1;
+  long long dp_budget = 1000000;
   std::string cost_model;
 };
 

@@ -115,6 +115,7 @@ struct KernelizeOptions {
   bool attach = true;
   int kinds = 3;
   bool front = true;       // also consider the front packing (R29)
+  long long dp_budget = 0; // Kernelize DP state budget (0 = none)
   int L = 0;               // local qubits (caps kernel sizes)
   u64 ls_set = 0;          // logical qubits at the forced LSB physical slots
 };

@@ -389,7 +389,23 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
     fd[i] = fd[i + 1] | (units[i].active ? 0 : units[i].qubits);
   }
   std::vector<St> cur(1);
+  // deterministic work budget (same on every rank, unlike a clock): when the
+  // DP would exceed it, Kernelize falls back to the cheaper of the front
+  // packing and OrderedKernelize (R29)
+  long long emitted = 0;
+  const long long budget = o.dp_budget > 0 ? o.dp_budget : LLONG_MAX;
+  auto fallback = [&]() {
+    KernelPlan best_plan = ordered;
+    if (o.front) {
+      KernelPlan fr = front_kernelize(seq, cm, o);
+      std::vector<int> ford;
+      for (auto &K : fr.kernels) ford.insert(ford.end(), K.gates.begin(), K.gates.end());
+      if (order_is_valid(seq, ford) && fr.total < best_plan.total) best_plan = fr;
+    }
+    return best_plan;
+  };
   for (int i = 0; i < nu; i++) {
+    if (emitted > budget) return fallback();
     const Unit &u = units[i];
     if (!getenv("ATLAS_DP_NOFUT")) {
       C.fut_q = fq[i + 1];
@@ -412,6 +428,7 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
     std::vector<St> next;
     std::unordered_map<u64, std::vector<int>> idx;
     auto emit = [&](St &&s) {
+      emitted++;
       C.close_dead_prefix(s);
       if ((int)next.size() >= 8 * T && T < INT_MAX / 16) {
         // keep the working set bounded inside an iteration as well (same
@@ -725,14 +742,8 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
   // the cheapest valid candidate: the DP, OrderedKernelize (Thm. dp-optimal
   // guarantees DP <= Ordered without pruning; pruning may worsen
   // it) and the commutation-aware front packing (R29)
-  KernelPlan best_plan = ordered;
+  KernelPlan best_plan = fallback();
   if (valid && kp.total <= best_plan.total) best_plan = kp;
-  if (o.front) {
-    KernelPlan fr = front_kernelize(seq, cm, o);
-    std::vector<int> ford;
-    for (auto &K : fr.kernels) ford.insert(ford.end(), K.gates.begin(), K.gates.end());
-    if (order_is_valid(seq, ford) && fr.total < best_plan.total) best_plan = fr;
-  }
   return best_plan;
 }
 

@@ -251,10 +251,13 @@ __device__ __forceinline__ void apply_op(typename Cplx<R>::T (&v)[1 << RB], cons
     }
     case OP_DENSE1: {
       T m[4];
+      // complex coefficients are 16-byte aligned pairs: one LDS.128 each
+      const double2 *c2 = reinterpret_cast<const double2 *>(coef + o.coef);
 #pragma unroll
       for (int i = 0; i < 4; i++) {
-        m[i].x = (R)coef[o.coef + 2 * i];
-        m[i].y = (R)coef[o.coef + 2 * i + 1];
+        const double2 cc = c2[i];
+        m[i].x = (R)cc.x;
+        m[i].y = (R)cc.y;
       }
       if (!CHK && (o.flags & OPF_REAL)) {
         switch (o.t0) {

@@ -443,6 +443,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
     ko.attach = C->opt.attach != 0;
     ko.kinds = C->opt.kinds;
     ko.front = C->opt.front != 0;
+    ko.dp_budget = C->opt.dp_budget;
     ko.L = L;
     ko.ls_set = ls_logical(mp.sigma, std::min(C->cm.ls_qubits, L));
     KernelPlan kp;

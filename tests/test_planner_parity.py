@@ -192,3 +192,35 @@ def test_greedy_baseline_is_fusion_up_to_5(tmp_path):
     pj = product_plan(c, 1, kernelizer=2)
     for k in pj["stages"][0]["kernels"]:
         assert k["kind"] == "fusion" and len(k["qubits"]) <= 5
+
+
+@pytest.mark.parametrize("fam", ["qft", "su2random", "ising", "qsvm", "wstate", "random"])
+def test_front_packing_valid(tmp_path, fam):
+    """The front packing (R29) yields kernels whose concatenation is
+    topologically equivalent to the stage (checked by the oracle's
+    verify_plan, Thm. dp-correct's notion) and whose reported cost
+    is the model cost of those kernels."""
+    n = 9
+    c = C.random_circuit(n, 40, 901, kinds=("H", "X", "CX", "CZ", "CP", "RZ", "U3", "SWAP", "CCX")) \
+        if fam == "random" else C.make(fam, n)
+    path, cm = model_json(tmp_path, qms=7, ls=2)
+    pj = product_plan(c, 1, kernelizer=3, cost_model=path)
+    seq = oracle_seq(c)
+    ks = pj["stages"][0]["kernels"]
+    errs, cost = P.verify_plan([k["gates"] for k in ks], [k["kind"] for k in ks], seq, cm,
+                               frozenset(range(2)), n, lift=True, check_constraint1=False)
+    assert errs == []
+    assert cost == pj["stages"][0]["kernel_cost"]
+
+
+def test_front_packing_cx_block_windows():
+    """An all-to-all CX block (su2random's entangler) needs one kernel per
+    window of q_max_shared - ls target qubits across all rows: 20 qubits, 2^12
+    tiles with 5 forced LSB qubits -> targets 1..11, 12..18, 19: 3 kernels."""
+    from workloads.circuits import Gate, Circuit
+    n = 20
+    c = Circuit(n, [Gate("CX", (i, j)) for i in range(n) for j in range(i + 1, n)])
+    pj = product_plan(c, 1, kernelizer=3, kinds=2)
+    assert len(pj["stages"][0]["kernels"]) == 3
+    pk = product_plan(c, 1, kernelizer=0, kinds=2)
+    assert len(pk["stages"][0]["kernels"]) == 3
