@@ -241,6 +241,7 @@ def run_atlas(args):
     for _ in range(args.warmup):
         sim.run()
     torch.cuda.synchronize()
+    jit_s = sim.plan_stats()["jit_us"] / 1e6  # first run: SHM kernel codegen + NVRTC
     sim.set_option("timing", 1)
     launches = []
     barrier()
@@ -353,7 +354,8 @@ def run_atlas(args):
         return
     pj = {"stages": stats["stages"], "remaps": stats["remaps"], "kernels": stats["kernels"],
           "fusion_kernels": stats["fusion_kernels"], "shm_kernels": stats["shm_kernels"],
-          "plan_s": round(plan_s, 3), "staging_exact": bool(stats["staging_exact"])}
+          "plan_s": round(plan_s, 3), "staging_exact": bool(stats["staging_exact"]),
+          "shm_jit": bool(extra.get("shm_jit", 1)), "jit_s": round(jit_s, 3)}
     line = {
         "metric": "amplitude-updates/s (circuit simulation)",
         "value": value, "unit": "amp-updates/s", "n_gpus": world, "steps": args.steps,

@@ -174,6 +174,11 @@ const char *atlas_last_error(void);
  *   "init"           1 = atlas_run starts from |0...0> [1]
  *   "timing"         1 = per-launch CUDA events (atlas_get_launches) [0]
  *   "shm_nbuf"       shared-memory tile buffers per CTA, 1..3 [1]
+ *   "shm_jit"        1 = each shared-memory launch runs a kernel generated
+ *                    from its lowered op program and compiled with NVRTC for
+ *                    sm_100a at the first atlas_run after a plan (cached per
+ *                    process by source); 0 = the generic interpreting
+ *                    kernel.  E_CUDA if libnvrtc.so.12 cannot be loaded. [1]
  *   "shm_rb"         register bits per phase for 2^12 tiles, 3 or 4 [4]
  *   "shm_direct_store"  last phase stores straight to HBM when coalesced [1]
  *   "shm_explicit_perm" execute permutation gates in registers when a
@@ -210,11 +215,23 @@ atlas_status atlas_nccl_unique_id(void *out128);
  * full length (call with cap = 0 to size). */
 atlas_status atlas_get_plan_json(atlas_ctx *ctx, char *buf, size_t cap, size_t *len);
 
-/* Plan summary, int64 values in this order (count = min(cap, 12)):
+/* Plan summary, int64 values in this order (count = min(cap, 13)):
  *   0 stages  1 staging cost x1000  2 kernels  3 fusion kernels  4 shm kernels
  *   5 kernel cost total  6 remaps  7 plan time (us)  8 staging exact (1/0)
- *   9 L  10 G  11 device launches per run */
+ *   9 L  10 G  11 device launches per run
+ *   12 time (us) the first atlas_run after this plan spent generating,
+ *      compiling (NVRTC) and loading the plan-specialised shared-memory
+ *      kernels (option "shm_jit"; 0 before that run) */
 atlas_status atlas_plan_stats(atlas_ctx *ctx, int64_t *out, int cap);
+
+/* The CUDA source of the plan-specialised kernel of shared-memory launch
+ * `index` (0-based, in launch order) of simulated rank `slot` (0 unless
+ * virtual_world): the lowered op program of P:L1964's shared-memory kernel
+ * written out as straight-line code (jit.cpp).  Host only; same buffer
+ * convention as atlas_get_plan_json.  E_INVALID if there is no such launch,
+ * E_ORDER before atlas_plan. */
+atlas_status atlas_get_jit_source(atlas_ctx *ctx, int slot, int index, char *buf,
+                                  size_t cap, size_t *len);
 
 /* Per-launch records of the last atlas_run (needs option "timing" = 1):
  * ms[i] device time, kind[i] (0 init, 1 fused, 2 shm, 3 pack, 4 exchange,

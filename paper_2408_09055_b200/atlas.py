@@ -33,6 +33,7 @@ SYMBOLS = [
     "atlas_set_state", "atlas_destroy", "atlas_last_error", "atlas_set_option_int",
     "atlas_set_option_str", "atlas_bind_buffers", "atlas_set_stream", "atlas_nccl_unique_id",
     "atlas_get_plan_json", "atlas_plan_stats", "atlas_get_launches", "atlas_remap_schedule",
+    "atlas_get_jit_source",
 ]
 
 
@@ -84,6 +85,7 @@ def lib():
             "atlas_plan_stats": [vp, vp, i32],
             "atlas_get_launches": [vp, vp, vp, vp, i32, ctypes.POINTER(i32)],
             "atlas_remap_schedule": [vp, i32, vp, i32, ctypes.POINTER(i32)],
+            "atlas_get_jit_source": [vp, i32, i32, vp, sz, ctypes.POINTER(sz)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -207,12 +209,22 @@ class Simulator:
         return json.loads(buf.value.decode())
 
     def plan_stats(self) -> dict:
-        v = (ctypes.c_int64 * 12)()
-        _check(lib().atlas_plan_stats(self._ctx, v, 12))
+        v = (ctypes.c_int64 * 13)()
+        _check(lib().atlas_plan_stats(self._ctx, v, 13))
         keys = ["stages", "staging_cost_x1000", "kernels", "fusion_kernels", "shm_kernels",
                 "kernel_cost", "remaps", "plan_us", "staging_exact", "L", "G",
-                "launches_per_run"]
+                "launches_per_run", "jit_us"]
         return dict(zip(keys, list(v)))
+
+    def jit_source(self, index: int, slot: int = 0) -> str:
+        """CUDA source of the plan-specialised kernel of shared-memory launch
+        `index` of simulated rank `slot` (host-only)."""
+        n = ctypes.c_size_t()
+        _check(lib().atlas_get_jit_source(self._ctx, slot, index, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(lib().atlas_get_jit_source(self._ctx, slot, index, buf, n.value + 1,
+                                          ctypes.byref(n)))
+        return buf.value.decode()
 
     def remap_schedule(self, stage: int):
         """This rank's transfers of the remap before `stage`:

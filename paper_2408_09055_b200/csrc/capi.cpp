@@ -15,6 +15,7 @@ void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count);
 void destroy(atlas_ctx *C);
 void nccl_unique_id(void *out);
 std::vector<Xfer> exchange_schedule(const atlas_ctx *C, int k, int r);
+std::string shm_jit_source_of(const atlas_ctx *C, int slot, int i);
 }  // namespace atlas
 
 using namespace atlas;
@@ -182,6 +183,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_direct_store") o.shm_direct_store = (int)v;
     else if (k == "shm_explicit_perm") o.shm_explicit_perm = (int)v;
     else if (k == "front") o.front = (int)v;
+    else if (k == "shm_jit") { o.shm_jit = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "dp_budget") o.dp_budget = (long long)v;
     else if (k == "shm_rb") { need(v == 3 || v == 4, ATLAS_E_INVALID, "shm_rb is 3 or 4"); o.shm_rb = (int)v; }
     else if (k == "shm_nbuf") { need(v >= 1 && v <= 3, ATLAS_E_INVALID, "shm_nbuf is 1, 2 or 3"); o.shm_nbuf = (int)v; }
@@ -253,7 +255,7 @@ atlas_status atlas_plan_stats(atlas_ctx *C, int64_t *out, int cap) {
   GUARD({
     need(C != nullptr && out != nullptr, ATLAS_E_INVALID, "NULL argument");
     need(C->planned, ATLAS_E_ORDER, "no plan");
-    int64_t v[12] = {0};
+    int64_t v[13] = {0};
     v[0] = C->sp.s;
     v[1] = (int64_t)llround(C->sp.cost * 1000);
     for (auto &kp : C->kplans) {
@@ -274,7 +276,23 @@ atlas_status atlas_plan_stats(atlas_ctx *C, int64_t *out, int cap) {
     for (auto &ln : C->prog[0])
       if (ln.type == L_FUSED || ln.type == L_SHM || ln.type == L_SCALE || ln.type == L_PACK) nl++;
     v[11] = nl;
-    for (int i = 0; i < cap && i < 12; i++) out[i] = v[i];
+    v[12] = (int64_t)C->jit_us;
+    for (int i = 0; i < cap && i < 13; i++) out[i] = v[i];
+  })
+}
+
+atlas_status atlas_get_jit_source(atlas_ctx *C, int slot, int index, char *buf, size_t cap,
+                                  size_t *len) {
+  GUARD({
+    need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
+    need(C->planned, ATLAS_E_ORDER, "no plan");
+    std::string s = shm_jit_source_of(C, slot, index);
+    if (len) *len = s.size();
+    if (buf && cap) {
+      size_t k = std::min(cap - 1, s.size());
+      memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
   })
 }
 

@@ -20,6 +20,7 @@ struct Launch {
   int64_t newpos_off = -1;   // L_PACK: offset into newpos blob (L ints)
   double sre = 1, sim = 0;   // L_SCALE
   int64_t bytes = 0;         // algorithmic HBM bytes
+  void *jit = nullptr;       // L_SHM: plan-specialised kernel (jit.cpp), or null
 };
 
 // Exchange of one remap (stage boundary k-1 -> k): swap the g' top local
@@ -66,6 +67,7 @@ struct Options {
   int shm_rb = 4;
   int shm_explicit_perm = 0;
   int front = 1;
+  int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter
   long long dp_budget = 1000000;
   std::string cost_model;
 };
@@ -108,7 +110,8 @@ struct atlas_ctx {
   std::vector<int> newpos;
 
   // device
-  bool dev_ready = false, blobs_ready = false;
+  bool dev_ready = false, blobs_ready = false, jit_ready = false;
+  double jit_us = 0;          // generation + NVRTC compile + load of the SHM kernels
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

@@ -1,0 +1,597 @@
+// jit.cpp -- plan-specialised shared-memory kernels (NVRTC, sm_100a).
+//
+// PAPER.md P:L1964 defines a shared-memory kernel as "load a micro-batch into
+// shared memory and apply the gates one by one".  The generic shm_kernel in
+// kernels.cu interprets the lowered op program (ShmOp/ShmPhase/DiagEnt/
+// PermTerm, device.h) for every tile: per op it loads a header, dispatches
+// on the op type and the target register bit, and loads the coefficients.
+// The circuit is fixed once atlas_plan returns, so this file turns the SAME
+// lowered program into straight-line CUDA for each launch: phases unrolled,
+// targets and element masks compile-time, gate coefficients literal constants,
+// permutation ops register renames, tile/thread conditions plain branches.
+// The generated kernel computes exactly what the interpreter computes (same
+// tile, phases, op order and arithmetic per element), so the interpreter
+// stays the reference for the JIT path in the GPU parity tests (option
+// shm_jit = 0 selects it).
+//
+// NVRTC is loaded at run time (libnvrtc.so.12 from the CUDA toolkit of this
+// image); the cubin is loaded with cudaLibraryLoadData.  Identical sources
+// are compiled once per process.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "ctx.h"
+
+namespace atlas {
+
+// ------------------------------------------------------------------- NVRTC
+namespace {
+typedef int nvrtcResult_;
+typedef void *nvrtcProgram_;
+struct NvrtcApi {
+  void *h = nullptr;
+  nvrtcResult_ (*create)(nvrtcProgram_ *, const char *, const char *, int, const char *const *,
+                         const char *const *) = nullptr;
+  nvrtcResult_ (*compile)(nvrtcProgram_, int, const char *const *) = nullptr;
+  nvrtcResult_ (*cubinSize)(nvrtcProgram_, size_t *) = nullptr;
+  nvrtcResult_ (*cubin)(nvrtcProgram_, char *) = nullptr;
+  nvrtcResult_ (*logSize)(nvrtcProgram_, size_t *) = nullptr;
+  nvrtcResult_ (*log)(nvrtcProgram_, char *) = nullptr;
+  nvrtcResult_ (*destroy)(nvrtcProgram_ *) = nullptr;
+  const char *(*err)(nvrtcResult_) = nullptr;
+};
+NvrtcApi g_nvrtc;
+std::mutex g_nvrtc_mu;
+
+void nvrtc_load() {
+  std::lock_guard<std::mutex> lk(g_nvrtc_mu);
+  if (g_nvrtc.h) return;
+  const char *names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
+  for (const char *nm : names) {
+    g_nvrtc.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+    if (g_nvrtc.h) break;
+  }
+  if (!g_nvrtc.h)
+    fail(ATLAS_E_CUDA, "cannot load libnvrtc.so.12 (needed by shm_jit=1): %s", dlerror());
+  auto S = [](const char *n) {
+    void *p = dlsym(g_nvrtc.h, n);
+    if (!p) fail(ATLAS_E_CUDA, "libnvrtc lacks %s", n);
+    return p;
+  };
+  g_nvrtc.create = (decltype(g_nvrtc.create))S("nvrtcCreateProgram");
+  g_nvrtc.compile = (decltype(g_nvrtc.compile))S("nvrtcCompileProgram");
+  g_nvrtc.cubinSize = (decltype(g_nvrtc.cubinSize))S("nvrtcGetCUBINSize");
+  g_nvrtc.cubin = (decltype(g_nvrtc.cubin))S("nvrtcGetCUBIN");
+  g_nvrtc.logSize = (decltype(g_nvrtc.logSize))S("nvrtcGetProgramLogSize");
+  g_nvrtc.log = (decltype(g_nvrtc.log))S("nvrtcGetProgramLog");
+  g_nvrtc.destroy = (decltype(g_nvrtc.destroy))S("nvrtcDestroyProgram");
+  g_nvrtc.err = (decltype(g_nvrtc.err))S("nvrtcGetErrorString");
+}
+
+struct JitEntry {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int smem = 0, nt = 0, attr_set = 0;
+};
+std::mutex g_cache_mu;
+std::unordered_map<std::string, JitEntry *> g_cache;  // source -> compiled kernel
+
+// --------------------------------------------------------------- emitter
+std::string lit(double d, bool f32) {
+  char b[64];
+  if (f32) {
+    float f = (float)d;
+    if (f == 0.0f) return "0.0f";
+    snprintf(b, sizeof b, "(%af)", (double)f);
+  } else {
+    if (d == 0.0) return "0.0";
+    snprintf(b, sizeof b, "(%a)", d);
+  }
+  return b;
+}
+
+std::string u64lit(uint64_t v) {
+  char b[32];
+  snprintf(b, sizeof b, "0x%llxull", (unsigned long long)v);
+  return b;
+}
+
+// y = M x over D register elements idx[0..D-1] (row-major complex M), the
+// terms ordered as in the interpreter (column by column), zero entries
+// dropped.
+void emit_block(std::ostringstream &o, int D, const int *idx, const double *m, bool f32,
+                const char *ind) {
+  o << ind << "{\n";
+  for (int c = 0; c < D; c++) o << ind << "  const T x" << c << " = v[" << idx[c] << "];\n";
+  for (int r = 0; r < D; r++) {
+    for (int part = 0; part < 2; part++) {
+      // part 0: re = sum mr*x.x - mi*x.y ; part 1: im = sum mr*x.y + mi*x.x
+      std::string acc;
+      for (int c = 0; c < D; c++) {
+        const double mr = m[2 * (r * D + c)], mi = m[2 * (r * D + c) + 1];
+        const double k0 = mr, k1 = part == 0 ? -mi : mi;
+        const std::string x0 = "x" + std::to_string(c) + (part == 0 ? ".x" : ".y");
+        const std::string x1 = "x" + std::to_string(c) + (part == 0 ? ".y" : ".x");
+        const std::pair<double, std::string> terms[2] = {{k0, x0}, {k1, x1}};
+        for (auto &t : terms) {
+          if (t.first == 0.0) continue;
+          if (acc.empty()) acc = lit(t.first, f32) + " * " + t.second;
+          else acc = "fma(" + lit(t.first, f32) + ", " + t.second + ", " + acc + ")";
+        }
+      }
+      if (acc.empty()) acc = f32 ? "0.0f" : "0.0";
+      o << ind << "  v[" << idx[r] << "]." << (part == 0 ? "x" : "y") << " = " << acc << ";\n";
+    }
+  }
+  o << ind << "}\n";
+}
+
+void emit_cmul_lit(std::ostringstream &o, int e, double re, double im, bool f32, const char *ind) {
+  if (re == 1.0 && im == 0.0) return;
+  if (im == 0.0) {
+    o << ind << "v[" << e << "].x *= " << lit(re, f32) << "; v[" << e << "].y *= " << lit(re, f32)
+      << ";\n";
+    return;
+  }
+  o << ind << "{ const T a = v[" << e << "]; v[" << e << "].x = " << lit(re, f32) << " * a.x - "
+    << lit(im, f32) << " * a.y; v[" << e << "].y = " << lit(re, f32) << " * a.y + " << lit(im, f32)
+    << " * a.x; }\n";
+}
+
+const int kDiagSel[11] = {0, 1, 2, 4, 8, 3, 5, 9, 6, 10, 12};
+
+}  // namespace
+
+int shm_nbuf_effective(int dtype, const ShmLaunch &sl);
+
+// The straight-line source of one shared-memory launch (same skeleton as
+// kernels.cu shm_kernel: ring of tile buffers filled with cp.async, register
+// phases, permuted stores, optional direct HBM store of the last phase).
+std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::string &name) {
+  const bool f32 = C->dt == ATLAS_C64;
+  const int K = sl.K, RB = sl.RB, NT = 1 << (K - RB), NE = 1 << RB, TILE = 1 << K;
+  const int nbuf = shm_nbuf_effective(f32 ? 1 : 0, sl);
+  const int esz = f32 ? 8 : 16;
+  auto swz = [&](int j) { return f32 ? swz_c64(j) : swz_c128(j); };
+  const ShmOp *ops = C->ops.data() + sl.ops_off;
+  const double *coef = C->coef.data() + sl.coef_off;
+  const ShmPhase *ph = C->phases.data() + sl.phase_off;
+  const DiagEnt *ents = C->ents.data() + sl.ent_off;
+  const PermTerm *terms = C->terms.data() + sl.term_off;
+  const int minb = (nbuf == 1 && (K - RB) >= 8 && (K - RB) <= 9 && (esz << K) <= 65536) ? 2 : 1;
+
+  // distinct thread-index tables: jt per register mask, store offsets per
+  // (register mask, permuted images)
+  std::vector<int> rmask(sl.nphase), jslot(sl.nphase), sslot(sl.nphase, -1);
+  std::vector<int> jmasks;
+  std::vector<std::pair<int, std::vector<uint16_t>>> smaps;
+  for (int p = 0; p < sl.nphase; p++) {
+    int m = 0;
+    for (int i = 0; i < RB; i++) m |= 1 << ph[p].rbit[i];
+    rmask[p] = m;
+    int js = -1;
+    for (size_t i = 0; i < jmasks.size(); i++)
+      if (jmasks[i] == m) js = (int)i;
+    if (js < 0) {
+      js = (int)jmasks.size();
+      jmasks.push_back(m);
+    }
+    jslot[p] = js;
+    if (ph[p].permuted) {
+      std::vector<uint16_t> img(ph[p].colimg, ph[p].colimg + K);
+      int ss = -1;
+      for (size_t i = 0; i < smaps.size(); i++)
+        if (smaps[i].first == m && smaps[i].second == img) ss = (int)i;
+      if (ss < 0) {
+        ss = (int)smaps.size();
+        smaps.push_back({m, img});
+      }
+      sslot[p] = ss;
+    }
+  }
+  const size_t off_jtab = (size_t)nbuf * TILE * esz;
+  const size_t off_stab = off_jtab + (size_t)jmasks.size() * NT * 4;
+  size_t off_btab = off_stab + (size_t)smaps.size() * NT * 2;
+  off_btab = (off_btab + 15) & ~(size_t)15;
+  const size_t smem = off_btab + 4 * 256 * 8;
+
+  std::ostringstream o;
+  o << "// generated by jit.cpp: shared-memory kernel, K=" << K << " RB=" << RB
+    << " phases=" << sl.nphase << " ops=" << sl.nops << "\n";
+  o << "typedef unsigned long long u64; typedef unsigned int u32; typedef unsigned short u16;\n";
+  o << (f32 ? "typedef float R; typedef float2 T;\n" : "typedef double R; typedef double2 T;\n");
+  o << "#define SMEM_BYTES " << smem << "\n";
+  o << "__device__ __forceinline__ int swz(int j) { return "
+    << (f32 ? "j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15)"
+            : "j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7)")
+    << "; }\n";
+  o << "__device__ __forceinline__ u64 pdep64(u64 v, u64 mask) { u64 r = 0; while (mask) { u64 lo = "
+       "mask & (~mask + 1); if (v & 1) r |= lo; v >>= 1; mask ^= lo; } return r; }\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
+    << "(T *__restrict__ st) {\n";
+  o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
+  o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
+  o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
+  o << "  u16 *stab = reinterpret_cast<u16 *>(smraw + " << off_stab << ");\n";
+  o << "  u64 *btab = reinterpret_cast<u64 *>(smraw + " << off_btab << ");\n";
+  o << "  const int tid = threadIdx.x;\n";
+  // tile-base deposit tables
+  o << "  for (int i = tid; i < 1024; i += " << NT << ") { const int c = i >> 8; u64 m = "
+    << u64lit(sl.nonactive) << "; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
+    << "pdep64((u64)(i & 255), m); }\n";
+  // per-thread tile indices of every distinct register mask
+  for (size_t js = 0; js < jmasks.size(); js++) {
+    o << "  { int jt = 0;";
+    int t = 0;
+    for (int b = 0; b < K; b++) {
+      if ((jmasks[js] >> b) & 1) continue;
+      o << " jt |= ((tid >> " << t << ") & 1) << " << b << ";";
+      t++;
+    }
+    o << " jtab[" << js * NT << " + tid] = ((u32)swz(jt) << 16) | (u32)jt; }\n";
+  }
+  for (size_t ss = 0; ss < smaps.size(); ss++) {
+    o << "  { u32 sa = 0;";
+    int t = 0;
+    for (int b = 0; b < K; b++) {
+      if ((smaps[ss].first >> b) & 1) continue;
+      o << " if ((tid >> " << t << ") & 1) sa ^= " << smaps[ss].second[b] << "u;";
+      t++;
+    }
+    o << " stab[" << ss * NT << " + tid] = (u16)sa; }\n";
+  }
+  // this thread's HBM offset inside a tile
+  o << "  u64 off_t = 0;";
+  for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) off_t |= " << u64lit(1ull << sl.act[i]) << ";";
+  o << "\n  const int sw_tid = swz(tid);\n";
+  o << "  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);\n";
+  o << "  __syncthreads();\n";
+  o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255] | btab[256 + ((tile >> 8) & 255)] | "
+       "btab[512 + ((tile >> 16) & 255)] | btab[768 + ((tile >> 24) & 255)]; };\n";
+  // per-register-element offsets (constant)
+  std::vector<uint64_t> itoff(NE);
+  for (int it = 0; it < NE; it++) {
+    uint64_t x = 0;
+    for (int i = 0; i < RB; i++)
+      if ((it >> i) & 1) x |= 1ull << sl.act[K - RB + i];
+    itoff[it] = x;
+  }
+  o << "  auto issue_load = [&](int bsel, u64 base) {\n    const T *g = st + base + off_t;\n";
+  for (int it = 0; it < NE; it++) {
+    o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (sw_tid ^ "
+      << swz(it * NT) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
+    if (!f32) o << "asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
+    else o << "asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
+  }
+  o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n  };\n";
+
+  const int last = sl.nphase - 1;
+  const bool ld = sl.last_direct != 0;
+  if (ld) {
+    o << "  u64 gthr = 0;\n  { const int jtl = (int)(jtab[" << jslot[last] * NT << " + tid] & 0xffffu);";
+    for (int b = 0; b < K; b++)
+      if (sl.lcol[b]) o << " if ((jtl >> " << b << ") & 1) gthr ^= " << u64lit(sl.lcol[b]) << ";";
+    o << " }\n";
+  }
+  o << "  u64 tile = blockIdx.x;\n  if (tile >= " << u64lit(sl.ntiles) << ") return;\n";
+  o << "  const u64 G = gridDim.x;\n";
+  for (int k = 0; k < nbuf - 1; k++)
+    o << "  { const u64 t = tile + " << k << "ull * G; if (t < " << u64lit(sl.ntiles)
+      << ") issue_load(" << k << ", tile_base(t)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); }\n";
+  o << "  int b = 0;\n";
+  o << "  for (; tile < " << u64lit(sl.ntiles) << "; tile += G) {\n";
+  o << "    const u64 base = tile_base(tile);\n";
+  o << "    { const u64 far = tile + " << (nbuf - 1) << "ull * G; const int fb = (b + " << (nbuf - 1)
+    << ") % " << nbuf << "; if (far < " << u64lit(sl.ntiles)
+    << ") issue_load(fb, tile_base(far)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");"
+    << " asm volatile(\"cp.async.wait_group " << (nbuf - 1) << ";\\n\" ::: \"memory\"); }\n";
+  o << "    __syncthreads();\n";
+  o << "    T *tb = buf + b * " << TILE << ";\n";
+  o << "    T v[" << NE << "];\n";
+  for (int p = 0; p < sl.nphase; p++) {
+    const ShmPhase &P = ph[p];
+    int sr[4] = {0, 0, 0, 0};
+    for (int i = 0; i < RB; i++) sr[i] = swz(1 << P.rbit[i]);
+    o << "    { // phase " << p << "\n";
+    o << "      const u32 jj = jtab[" << jslot[p] * NT << " + tid]; const int jt = (int)(jj & 0xffffu); "
+      << "const int sj = (int)(jj >> 16); (void)jt;\n";
+    for (int e = 0; e < NE; e++) {
+      int a = 0;
+      for (int i = 0; i < RB; i++)
+        if ((e >> i) & 1) a ^= sr[i];
+      o << "      v[" << e << "] = tb[sj ^ " << a << "];\n";
+    }
+    for (int oi = P.op_begin; oi < P.op_end; oi++) {
+      const ShmOp &op = ops[oi];
+      const double *c = coef + op.coef;
+      if (op.type == OP_DIAG) {
+        const int sel = kDiagSel[op.t0];
+        const int eb = (int)op.base_mask, ee = (int)op.base_val;
+        if (eb == ee) {
+          for (int e = 0; e < NE; e++)
+            if ((e & sel) == sel) emit_cmul_lit(o, e, c[0], c[1], f32, "      ");
+          continue;
+        }
+        o << "      { double fx = " << lit(c[0], false) << ", fy = " << lit(c[1], false) << ";\n";
+        for (int i = eb; i < ee; i++) {
+          const DiagEnt &d = ents[i];
+          o << "        if (((jt & " << d.thr_mask << ") == " << d.thr_val << ")";
+          if (d.has_base) o << " && ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val) << ")";
+          o << ") { const double nx = fx * " << lit(d.re, false) << " - fy * " << lit(d.im, false)
+            << "; fy = fx * " << lit(d.im, false) << " + fy * " << lit(d.re, false) << "; fx = nx; }\n";
+        }
+        o << "        T f; f.x = (R)fx; f.y = (R)fy;\n";
+        for (int e = 0; e < NE; e++)
+          if ((e & sel) == sel)
+            o << "        { const T a = v[" << e << "]; v[" << e << "].x = f.x * a.x - f.y * a.y; v[" << e
+              << "].y = f.x * a.y + f.y * a.x; }\n";
+        o << "      }\n";
+        continue;
+      }
+      const bool full = (op.flags & OPF_FULL) != 0;
+      const unsigned em = full ? 0xffffu : op.emask;
+      const char *ind = "      ";
+      if (!full) {
+        o << "      if (";
+        bool any = false;
+        if (op.base_mask) {
+          o << "((base & " << u64lit(op.base_mask) << ") == " << u64lit(op.base_val) << ")";
+          any = true;
+        }
+        if (op.thr_mask) {
+          if (any) o << " && ";
+          o << "((jt & " << op.thr_mask << ") == " << op.thr_val << ")";
+          any = true;
+        }
+        if (!any) o << "true";
+        o << ") {\n";
+        ind = "        ";
+      }
+      switch (op.type) {
+        case OP_PHASE:
+          for (int e = 0; e < NE; e++)
+            if ((em >> e) & 1) emit_cmul_lit(o, e, c[0], c[1], f32, ind);
+          break;
+        case OP_DENSE1: {
+          const int tb = op.t0;
+          for (int e = 0; e < NE; e++) {
+            if (e & (1 << tb)) continue;
+            if (!((em >> e) & 1)) continue;
+            const int idx[2] = {e, e | (1 << tb)};
+            emit_block(o, 2, idx, c, f32, ind);
+          }
+          break;
+        }
+        case OP_PERM1: {
+          const int tb = op.t0;
+          for (int e = 0; e < NE; e++) {
+            if (e & (1 << tb)) continue;
+            if (!((em >> e) & 1)) continue;
+            o << ind << "{ const T a = v[" << e << "]; v[" << e << "] = v[" << (e | (1 << tb)) << "]; v["
+              << (e | (1 << tb)) << "] = a; }\n";
+          }
+          break;
+        }
+        default: {  // OP_DENSE2
+          const int t0 = op.t0, t1 = op.t1;
+          for (int e = 0; e < NE; e++) {
+            if (e & ((1 << t0) | (1 << t1))) continue;
+            if (!((em >> e) & 1)) continue;
+            const int idx[4] = {e, e | (1 << t0), e | (1 << t1), e | (1 << t0) | (1 << t1)};
+            emit_block(o, 4, idx, c, f32, ind);
+          }
+        }
+      }
+      if (!full) o << "      }\n";
+    }
+    if (ld && p == last) {
+      uint64_t limg[4] = {0, 0, 0, 0};
+      for (int i = 0; i < RB; i++) limg[i] = sl.lcol[P.rbit[i]];
+      o << "      u64 cg = gthr;\n";
+      if (P.permuted) {
+        o << "      cg ^= " << u64lit(sl.lc0) << ";\n";
+        for (int i = P.term_begin; i < P.term_end; i++)
+          o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
+            << ") cg ^= " << u64lit(terms[i].gvec) << ";\n";
+      }
+      for (int e = 0; e < NE; e++) {
+        uint64_t x = 0;
+        for (int i = 0; i < RB; i++)
+          if ((e >> i) & 1) x ^= limg[i];
+        o << "      st[base | (cg ^ " << u64lit(x) << ")] = v[" << e << "];\n";
+      }
+      o << "    }\n";
+      break;
+    }
+    if (P.permuted) {
+      o << "      u32 cb = " << P.c0_swz << "u;\n";
+      for (int i = P.term_begin; i < P.term_end; i++)
+        o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
+          << ") cb ^= " << terms[i].vec_swz << "u;\n";
+      o << "      const int s0 = (int)(stab[" << sslot[p] * NT << " + tid] ^ cb);\n";
+      o << "      __syncthreads();\n";
+      for (int e = 0; e < NE; e++) {
+        int a = 0;
+        for (int i = 0; i < RB; i++)
+          if ((e >> i) & 1) a ^= P.colimg[P.rbit[i]];
+        o << "      tb[s0 ^ " << a << "] = v[" << e << "];\n";
+      }
+    } else {
+      for (int e = 0; e < NE; e++) {
+        int a = 0;
+        for (int i = 0; i < RB; i++)
+          if ((e >> i) & 1) a ^= sr[i];
+        o << "      tb[sj ^ " << a << "] = v[" << e << "];\n";
+      }
+    }
+    o << "      __syncthreads();\n    }\n";
+  }
+  if (!ld) {
+    o << "    { T *g = st + base + off_t;\n";
+    for (int it = 0; it < NE; it++)
+      o << "      g[" << u64lit(itoff[it]) << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
+    o << "    }\n";
+  }
+  o << "    __syncthreads();\n";
+  o << "    b = (b + 1) % " << nbuf << ";\n";
+  o << "  }\n}\n";
+  return o.str();
+}
+
+size_t shm_jit_smem(const std::string &src) {
+  const char *p = strstr(src.c_str(), "#define SMEM_BYTES ");
+  return p ? (size_t)strtoull(p + 19, nullptr, 10) : 0;
+}
+
+// Compile (NVRTC, sm_100a) every source not yet in the process cache; the
+// distinct sources are spread over host threads.
+static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &srcs,
+                                               const std::vector<std::string> &names) {
+  nvrtc_load();
+  std::vector<JitEntry *> out(srcs.size(), nullptr);
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (size_t i = 0; i < srcs.size(); i++) {
+      auto it = g_cache.find(srcs[i]);
+      if (it != g_cache.end()) out[i] = it->second;
+      else todo.push_back(i);
+    }
+  }
+  std::vector<std::string> errs(srcs.size());
+  std::vector<std::vector<char>> cubins(srcs.size());
+  std::atomic<size_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      const size_t w = next.fetch_add(1);
+      if (w >= todo.size()) return;
+      const size_t i = todo[w];
+      nvrtcProgram_ prog = nullptr;
+      int r = g_nvrtc.create(&prog, srcs[i].c_str(), (names[i] + ".cu").c_str(), 0, nullptr, nullptr);
+      if (r != 0) {
+        errs[i] = std::string("nvrtcCreateProgram: ") + g_nvrtc.err(r);
+        continue;
+      }
+      const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-default-device"};
+      r = g_nvrtc.compile(prog, 4, opts);
+      if (r != 0) {
+        size_t ls = 0;
+        g_nvrtc.logSize(prog, &ls);
+        std::string log(ls, '\0');
+        g_nvrtc.log(prog, &log[0]);
+        errs[i] = std::string("nvrtcCompileProgram: ") + g_nvrtc.err(r) + "\n" + log.substr(0, 2000);
+        g_nvrtc.destroy(&prog);
+        continue;
+      }
+      size_t cs = 0;
+      g_nvrtc.cubinSize(prog, &cs);
+      cubins[i].resize(cs);
+      g_nvrtc.cubin(prog, cubins[i].data());
+      g_nvrtc.destroy(&prog);
+    }
+  };
+  unsigned nth = std::thread::hardware_concurrency();
+  if (nth == 0) nth = 4;
+  nth = std::min<unsigned>(nth, 32);
+  nth = std::min<unsigned>(nth, (unsigned)std::max<size_t>(todo.size(), 1));
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nth; t++) th.emplace_back(worker);
+  worker();
+  for (auto &t : th) t.join();
+  for (size_t i : todo)
+    if (!errs[i].empty()) fail(ATLAS_E_CUDA, "shm_jit: %s", errs[i].c_str());
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (size_t i : todo) {
+    auto it = g_cache.find(srcs[i]);
+    if (it != g_cache.end()) {  // same source twice in this batch
+      out[i] = it->second;
+      continue;
+    }
+    JitEntry *E = new JitEntry();
+    cudaError_t e = cudaLibraryLoadData(&E->lib, cubins[i].data(), nullptr, nullptr, 0, nullptr,
+                                        nullptr, 0);
+    if (e != cudaSuccess) fail(ATLAS_E_CUDA, "cudaLibraryLoadData: %s", cudaGetErrorString(e));
+    e = cudaLibraryGetKernel(&E->kern, E->lib, names[i].c_str());
+    if (e != cudaSuccess) fail(ATLAS_E_CUDA, "cudaLibraryGetKernel: %s", cudaGetErrorString(e));
+    E->smem = (int)shm_jit_smem(srcs[i]);
+    g_cache[srcs[i]] = E;
+    out[i] = E;
+  }
+  return out;
+}
+
+// Generate and compile the specialised kernel of every L_SHM launch of the
+// plan (all simulated ranks); Launch::jit points at the cache entry.
+void shm_jit_prepare(atlas_ctx *C) {
+  std::vector<std::string> srcs, names;
+  std::vector<Launch *> lns;
+  for (auto &P : C->prog)
+    for (auto &ln : P)
+      if (ln.type == L_SHM) {
+        // the name does not enter the cache key: it is derived from the body
+        std::string body = shm_jit_source(C, ln.sl, "atlas_shm_jit");
+        const size_t h = std::hash<std::string>()(body);
+        char nm[64];
+        snprintf(nm, sizeof nm, "atlas_shm_%016zx", h);
+        std::string s = body;
+        const size_t at = s.find("atlas_shm_jit");
+        s.replace(at, strlen("atlas_shm_jit"), nm);
+        srcs.push_back(s);
+        names.push_back(nm);
+        lns.push_back(&ln);
+      }
+  if (srcs.empty()) return;
+  auto ents = jit_compile_all(srcs, names);
+  for (size_t i = 0; i < lns.size(); i++) lns[i]->jit = ents[i];
+}
+
+static int g_nsms = 0;
+
+cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s) {
+  JitEntry *E = (JitEntry *)jit;
+  const int NT = 1 << (sl.K - sl.RB);
+  if (E->attr_set < E->smem) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)E->kern,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, E->smem);
+    if (e != cudaSuccess) return e;
+    E->attr_set = E->smem;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)E->kern, NT, E->smem);
+    if (e != cudaSuccess) return e;
+    E->nt = occ < 1 ? 1 : occ;
+  }
+  if (!g_nsms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_nsms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_nsms <= 0) g_nsms = 148;
+  }
+  uint64_t grid = (uint64_t)g_nsms * E->nt;
+  if (grid > sl.ntiles) grid = sl.ntiles;
+  void *args[] = {&st};
+  return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
+                          (size_t)E->smem, s);
+}
+
+// source of launch i of slot s (tests / inspection: atlas_get_jit_source)
+std::string shm_jit_source_of(const atlas_ctx *C, int slot, int i) {
+  if (slot < 0 || slot >= (int)C->prog.size()) fail(ATLAS_E_INVALID, "slot out of range");
+  int j = 0;
+  for (auto &ln : C->prog[slot])
+    if (ln.type == L_SHM && j++ == i) return shm_jit_source(C, ln.sl, "atlas_shm_jit");
+  fail(ATLAS_E_INVALID, "no shared-memory launch %d", i);
+  return "";
+}
+
+}  // namespace atlas

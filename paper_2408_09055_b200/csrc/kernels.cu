@@ -749,6 +749,20 @@ static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const ShmOp *ops,
 
 int shm_register_bits(int K) { return K >= 9 ? 4 : K - 5; }
 
+// number of tile buffers launch_shm_t picks for a launch (jit.cpp mirrors it)
+int shm_nbuf_effective(int dtype, const ShmLaunch &sl) {
+  const bool F64 = dtype == 0;
+  if (sl.K <= 10) return 2;
+  if (sl.K == 11) return sl.nbuf == 1 ? 1 : 2;
+  if (sl.K == 12) {
+    if (sl.RB == 3) return 1;
+    const int esz = F64 ? 16 : 8;
+    if (sl.nbuf == 3 && shm_smem_layout(esz << 12, 3, sl, 256, 16).total <= 232448) return 3;
+    return sl.nbuf == 1 ? 1 : 2;
+  }
+  return F64 ? 1 : 2;
+}
+
 cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *ops,
                        const double *coef, const ShmPhase *ph, const DiagEnt *ents,
                        const PermTerm *terms, cudaStream_t s) {

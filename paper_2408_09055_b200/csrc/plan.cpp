@@ -1003,6 +1003,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
   }
   C->planned = true;
   C->blobs_ready = false;
+  C->jit_ready = false;
   C->plan_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
 }
 

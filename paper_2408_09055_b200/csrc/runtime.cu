@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -29,6 +30,8 @@ cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const in
                            const int *newpos_dev, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
+void shm_jit_prepare(atlas_ctx *C);
+cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s);
 
 #define CK(x)                                                                              \
   do {                                                                                     \
@@ -247,6 +250,14 @@ void run(atlas_ctx *C) {
   if (!C->planned) fail(ATLAS_E_ORDER, "atlas_run before atlas_plan");
   ensure_device(C);
   ensure_blobs(C);
+  if (!C->jit_ready) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (auto &P : C->prog)
+      for (auto &ln : P) ln.jit = nullptr;
+    if (C->opt.shm_jit) shm_jit_prepare(C);
+    C->jit_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    C->jit_ready = true;
+  }
   const int dt = C->dt == ATLAS_C128 ? 0 : 1;
   const bool timing = C->opt.timing != 0;
   C->launch_ms.clear();
@@ -311,6 +322,10 @@ void run(atlas_ctx *C) {
         switch (ln.type) {
           case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
           case L_SHM:
+            if (ln.jit) {
+              CK(launch_shm_jit(ln.jit, st, ln.sl, C->stream));
+              break;
+            }
             CK(launch_shm(dt, st, ln.sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                           (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
                           (const PermTerm *)C->d_terms, C->stream));

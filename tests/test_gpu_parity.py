@@ -198,3 +198,28 @@ def test_shm_lowering_variants(fam, opt):
     c = C.random_circuit(13, 150, 77) if fam == "random" else C.make(fam, 13)
     psi, _ = run(c, **opt)
     check(psi, O.simulate(c))
+
+
+@pytest.mark.parametrize("fam", ["su2random", "qsvm", "ising", "qft", "random"])
+@pytest.mark.parametrize("world", [1, 4])
+def test_shm_interpreter_vs_jit(fam, world):
+    """The plan-specialised SHM kernels (option shm_jit=1, jit.cpp) and the
+    generic interpreting kernel (shm_jit=0) run the same lowered program:
+    both match the oracle, and each other to rounding."""
+    c = C.random_circuit(14, 160, 91) if fam == "random" else C.make(fam, 14)
+    ref = O.simulate(c)
+    a, _ = run(c, world=world, shm_jit=0)
+    b, _ = run(c, world=world, shm_jit=1)
+    check(a, ref)
+    check(b, ref)
+    assert np.abs(a - b).max() <= 1e-12
+
+
+@pytest.mark.parametrize("fam", ["su2random", "random"])
+@pytest.mark.parametrize("opt", [{"shm_rb": 3}, {"shm_nbuf": 2}, {"shm_direct_store": 0},
+                                 {"shm_explicit_perm": 1}])
+def test_shm_interpreter_variants(fam, opt):
+    """The interpreting kernel stays covered under every lowering variant."""
+    c = C.random_circuit(13, 150, 78) if fam == "random" else C.make(fam, 13)
+    psi, _ = run(c, shm_jit=0, **opt)
+    check(psi, O.simulate(c))
