@@ -286,16 +286,33 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   }
   o << "  u64 tile = blockIdx.x;\n  if (tile >= " << u64lit(sl.ntiles) << ") return;\n";
   o << "  const u64 G = gridDim.x;\n";
-  for (int k = 0; k < nbuf - 1; k++)
-    o << "  { const u64 t = tile + " << k << "ull * G; if (t < " << u64lit(sl.ntiles)
-      << ") issue_load(" << k << ", tile_base(t)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); }\n";
+  // early = one tile buffer: the next tile's load is issued as soon as every
+  // thread has read the current tile out of shared memory for the last time
+  // (the last phase's gather, or the copy-out), so it overlaps the last
+  // phase's arithmetic and the HBM stores; the other CTA of the SM covers
+  // the rest.
+  const bool early = nbuf == 1;
+  const std::string NTL = u64lit(sl.ntiles);
+  const std::string next_issue =
+      "{ const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
+  if (early) {
+    o << "  issue_load(0, tile_base(tile));\n";
+  } else {
+    for (int k = 0; k < nbuf - 1; k++)
+      o << "  { const u64 t = tile + " << k << "ull * G; if (t < " << NTL
+        << ") issue_load(" << k << ", tile_base(t)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); }\n";
+  }
   o << "  int b = 0;\n";
-  o << "  for (; tile < " << u64lit(sl.ntiles) << "; tile += G) {\n";
+  o << "  for (; tile < " << NTL << "; tile += G) {\n";
   o << "    const u64 base = tile_base(tile);\n";
-  o << "    { const u64 far = tile + " << (nbuf - 1) << "ull * G; const int fb = (b + " << (nbuf - 1)
-    << ") % " << nbuf << "; if (far < " << u64lit(sl.ntiles)
-    << ") issue_load(fb, tile_base(far)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");"
-    << " asm volatile(\"cp.async.wait_group " << (nbuf - 1) << ";\\n\" ::: \"memory\"); }\n";
+  if (early) {
+    o << "    asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+  } else {
+    o << "    { const u64 far = tile + " << (nbuf - 1) << "ull * G; const int fb = (b + " << (nbuf - 1)
+      << ") % " << nbuf << "; if (far < " << NTL
+      << ") issue_load(fb, tile_base(far)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");"
+      << " asm volatile(\"cp.async.wait_group " << (nbuf - 1) << ";\\n\" ::: \"memory\"); }\n";
+  }
   o << "    __syncthreads();\n";
   o << "    T *tb = buf + b * " << TILE << ";\n";
   o << "    T v[" << NE << "];\n";
@@ -312,6 +329,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
         if ((e >> i) & 1) a ^= sr[i];
       o << "      v[" << e << "] = tb[sj ^ " << a << "];\n";
     }
+    if (early && ld && p == last) o << "      __syncthreads();\n      " << next_issue << "\n";
     for (int oi = P.op_begin; oi < P.op_end; oi++) {
       const ShmOp &op = ops[oi];
       const double *c = coef + op.coef;
@@ -439,11 +457,17 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   }
   if (!ld) {
     o << "    { T *g = st + base + off_t;\n";
-    for (int it = 0; it < NE; it++)
-      o << "      g[" << u64lit(itoff[it]) << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
+    if (early) {
+      for (int it = 0; it < NE; it++) o << "      v[" << it << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
+      o << "      __syncthreads();\n      " << next_issue << "\n";
+      for (int it = 0; it < NE; it++) o << "      g[" << u64lit(itoff[it]) << "] = v[" << it << "];\n";
+    } else {
+      for (int it = 0; it < NE; it++)
+        o << "      g[" << u64lit(itoff[it]) << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
+    }
     o << "    }\n";
   }
-  o << "    __syncthreads();\n";
+  if (!early) o << "    __syncthreads();\n";
   o << "    b = (b + 1) % " << nbuf << ";\n";
   o << "  }\n}\n";
   return o.str();

@@ -971,7 +971,6 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
             int rm = 0;
             for (int i = 0; i < RB; i++) rm |= 1 << lp.rbit[i];
             const int lowm = (1 << std::min(5, K_ - RB)) - 1;
-            ln.sl.last_direct = C->opt.shm_direct_store && !(rm & lowm);
             const bool perm = lp.permuted != 0;
             auto dep = [&](u32 x) {
               u64 r = 0;
@@ -979,6 +978,14 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                 if ((x >> b) & 1) r |= 1ull << act[b];
               return r;
             };
+            // the 32 lanes of a warp must write one contiguous 512-B run:
+            // tile bits 0..4 are physical slots 0..4 and the folded map sends
+            // them into that span (it is invertible, so onto it)
+            bool coalesced = K_ - RB >= 5 && dep(0x1fu) == 0x1full;
+            if (perm)
+              for (int b = 0; b < 5 && coalesced; b++)
+                if (lb.col[b] & ~0x1fu) coalesced = false;
+            ln.sl.last_direct = C->opt.shm_direct_store && !(rm & lowm) && coalesced;
             for (int b = 0; b < 16; b++)
               ln.sl.lcol[b] = b < K_ ? dep(perm ? lb.col[b] : (1u << b)) : 0;
             ln.sl.lc0 = perm ? dep(lb.c0) : 0;
