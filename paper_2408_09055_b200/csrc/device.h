@@ -95,7 +95,12 @@ struct ShmPhase {
   int32_t op_begin, op_end;
   uint16_t colimg[16];         // store image of each tile bit (swizzled)
   uint32_t c0_swz;             // swizzled constant of the store map
-  int32_t permuted;            // 0: identity store (colimg/c0 unused)
+  int16_t permuted;            // 0: identity store (colimg/c0 unused)
+  // tile bits of thread bits 0..W-1 (W = 3 fp64 / 4 fp32: the lanes of one
+  // shared-memory wavefront), one nibble each, 0xF = unused; 0xFFFF = the
+  // default (non-register tile bits in ascending order).  Chosen so that the
+  // gather and the permuted store of the phase are bank-conflict free.
+  uint16_t qlane;
   int32_t term_begin, term_end;
 };
 static_assert(sizeof(ShmPhase) == 72, "ShmPhase layout");

@@ -174,28 +174,29 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   // distinct thread-index tables: jt per register mask, store offsets per
   // (register mask, permuted images)
   std::vector<int> rmask(sl.nphase), jslot(sl.nphase), sslot(sl.nphase, -1);
-  std::vector<int> jmasks;
+  std::vector<int> jmasks;  // register mask | qlane << 16
   std::vector<std::pair<int, std::vector<uint16_t>>> smaps;
   for (int p = 0; p < sl.nphase; p++) {
     int m = 0;
     for (int i = 0; i < RB; i++) m |= 1 << ph[p].rbit[i];
     rmask[p] = m;
+    const int key = m | ((int)ph[p].qlane << 16);
     int js = -1;
     for (size_t i = 0; i < jmasks.size(); i++)
-      if (jmasks[i] == m) js = (int)i;
+      if (jmasks[i] == key) js = (int)i;
     if (js < 0) {
       js = (int)jmasks.size();
-      jmasks.push_back(m);
+      jmasks.push_back(key);
     }
     jslot[p] = js;
     if (ph[p].permuted) {
       std::vector<uint16_t> img(ph[p].colimg, ph[p].colimg + K);
       int ss = -1;
-      for (size_t i = 0; i < smaps.size(); i++)
-        if (smaps[i].first == m && smaps[i].second == img) ss = (int)i;
+        for (size_t i = 0; i < smaps.size(); i++)
+        if (smaps[i].first == key && smaps[i].second == img) ss = (int)i;
       if (ss < 0) {
         ss = (int)smaps.size();
-        smaps.push_back({m, img});
+        smaps.push_back({key, img});
       }
       sslot[p] = ss;
     }
@@ -230,25 +231,34 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "  for (int i = tid; i < 1024; i += " << NT << ") { const int c = i >> 8; u64 m = "
     << u64lit(sl.nonactive) << "; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
     << "pdep64((u64)(i & 255), m); }\n";
-  // per-thread tile indices of every distinct register mask
+  // per-thread tile indices of every distinct (register mask, lane order):
+  // thread bit i -> tile bit order[i] (kernels.cu shm_kernel prologue)
+  auto thread_order = [&](int key) {
+    const int m = key & 0xffff, q = (key >> 16) & 0xffff;
+    std::vector<int> ord;
+    int used = m;
+    if (q != 0xffff)
+      for (int i = 0; i < 4; i++) {
+        const int nb = (q >> (4 * i)) & 15;
+        if (nb == 15) break;
+        ord.push_back(nb);
+        used |= 1 << nb;
+      }
+    for (int b = 0; b < K; b++)
+      if (!((used >> b) & 1)) ord.push_back(b);
+    return ord;
+  };
   for (size_t js = 0; js < jmasks.size(); js++) {
     o << "  { int jt = 0;";
-    int t = 0;
-    for (int b = 0; b < K; b++) {
-      if ((jmasks[js] >> b) & 1) continue;
-      o << " jt |= ((tid >> " << t << ") & 1) << " << b << ";";
-      t++;
-    }
+    const std::vector<int> ord = thread_order(jmasks[js]);
+    for (size_t t = 0; t < ord.size(); t++) o << " jt |= ((tid >> " << t << ") & 1) << " << ord[t] << ";";
     o << " jtab[" << js * NT << " + tid] = ((u32)swz(jt) << 16) | (u32)jt; }\n";
   }
   for (size_t ss = 0; ss < smaps.size(); ss++) {
     o << "  { u32 sa = 0;";
-    int t = 0;
-    for (int b = 0; b < K; b++) {
-      if ((smaps[ss].first >> b) & 1) continue;
-      o << " if ((tid >> " << t << ") & 1) sa ^= " << smaps[ss].second[b] << "u;";
-      t++;
-    }
+    const std::vector<int> ord = thread_order(smaps[ss].first);
+    for (size_t t = 0; t < ord.size(); t++)
+      o << " if ((tid >> " << t << ") & 1) sa ^= " << smaps[ss].second[ord[t]] << "u;";
     o << " stab[" << ss * NT << " + tid] = (u16)sa; }\n";
   }
   // this thread's HBM offset inside a tile

@@ -429,9 +429,17 @@ __global__ void __launch_bounds__(1 << (K - RB), (ShmMinBlocks<R, K, RB, NBUF>::
     int rmask = 0;
 #pragma unroll
     for (int i = 0; i < RB; i++) rmask |= 1 << ph[p].rbit[i];
-    int jt = 0, t = tid;
+    int jt = 0, t = tid, used = rmask;
+    if (ph[p].qlane != 0xffff)
+      for (int i = 0; i < 4; i++) {
+        const int nb = (ph[p].qlane >> (4 * i)) & 15;
+        if (nb == 15) break;
+        jt |= (t & 1) << nb;
+        t >>= 1;
+        used |= 1 << nb;
+      }
     for (int b = 0; b < K; b++) {
-      if ((rmask >> b) & 1) continue;
+      if ((used >> b) & 1) continue;
       jt |= (t & 1) << b;
       t >>= 1;
     }

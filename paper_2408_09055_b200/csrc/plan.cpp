@@ -960,6 +960,66 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               }
               ph.term_end = (int32_t)(C->terms.size() - ln.sl.term_off);
             }
+            {
+              // lanes of one shared-memory wavefront (thread bits 0..W-1):
+              // pick W non-register tile bits whose swizzled bank groups are
+              // independent for the gather (identity addresses) and for the
+              // permuted store (images colimg); default ascending order
+              // when it already is conflict-free
+              const int W = C->dt == ATLAS_C128 ? 3 : 4;
+              const u32 wm = (1u << W) - 1;
+              std::vector<int> nr;
+              for (int b = 0; b < K_; b++)
+                if (!((rm >> b) & 1)) nr.push_back(b);
+              auto rank_of = [&](const std::vector<u32> &vs) {
+                u32 basis[16] = {0};
+                int r = 0;
+                for (u32 v : vs) {
+                  for (int bit = 15; bit >= 0 && v; bit--)
+                    if ((v >> bit) & 1) {
+                      if (!basis[bit]) {
+                        basis[bit] = v;
+                        r++;
+                        v = 0;
+                      } else {
+                        v ^= basis[bit];
+                      }
+                    }
+                }
+                return r;
+              };
+              auto cost = [&](const std::vector<int> &sel) {
+                std::vector<u32> ld, st;
+                for (int b : sel) {
+                  ld.push_back(swzh(1u << b) & wm);
+                  st.push_back((ph.permuted ? (u32)ph.colimg[b] : swzh(1u << b)) & wm);
+                }
+                return (1 << (W - rank_of(ld))) + (1 << (W - rank_of(st)));
+              };
+              ph.qlane = 0xffff;
+              if ((int)nr.size() >= W) {
+                std::vector<int> def(nr.begin(), nr.begin() + W);
+                int best = cost(def);
+                std::vector<int> bsel;
+                const int nn = (int)nr.size();
+                for (u32 m = 0; m < (1u << nn) && best > 2; m++) {
+                  if (popc((u64)m) != W) continue;
+                  std::vector<int> sel;
+                  for (int i = 0; i < nn; i++)
+                    if ((m >> i) & 1) sel.push_back(nr[i]);
+                  const int c = cost(sel);
+                  if (c < best) {
+                    best = c;
+                    bsel = sel;
+                  }
+                }
+                if (!bsel.empty()) {
+                  u32 q = 0xffff;
+                  for (int i = 0; i < W; i++) q = (q & ~(15u << (4 * i))) | ((u32)bsel[i] << (4 * i));
+                  ph.qlane = (uint16_t)q;
+                }
+              }
+            }
             C->phases.push_back(ph);
           }
           if (sl == 0) C->kplans[k].kernels[&K - &kp.kernels[0]].nphase = (int)phs.size();
@@ -986,6 +1046,8 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               for (int b = 0; b < 5 && coalesced; b++)
                 if (lb.col[b] & ~0x1fu) coalesced = false;
             ln.sl.last_direct = C->opt.shm_direct_store && !(rm & lowm) && coalesced;
+            // the direct store needs lanes = tile bits 0..4 in order
+            if (ln.sl.last_direct) C->phases.back().qlane = 0xffff;
             for (int b = 0; b < 16; b++)
               ln.sl.lcol[b] = b < K_ ? dep(perm ? lb.col[b] : (1u << b)) : 0;
             ln.sl.lc0 = perm ? dep(lb.c0) : 0;
