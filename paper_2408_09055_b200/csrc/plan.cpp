@@ -76,7 +76,12 @@ struct Pre {
   // c^(sum_k e_k * prod_{b in m_k} j_b) over monomials (m_k, e_k) of the
   // register-phase tile index j (|m_k| <= 2), times the base selectors
   bool conj = false;
-  std::vector<std::pair<u32, int>> mono;
+  struct Mono {
+    u32 m;       // tile bits of the monomial
+    int e;       // exponent of c
+    u64 bm, bv;  // tile-base condition under which it applies (0, 0: always)
+  };
+  std::vector<Mono> mono;
 };
 
 // A register phase under construction.  items: (0, dense ops) or
@@ -99,46 +104,77 @@ struct PhaseB {
   // index j the registers hold (D pi = pi D', D' = pi^-1 D pi): each tile
   // selector (x_a == v) becomes (parity(j & row_a(A)) ^ c0_a == v).
   // Supported: one selector with |row| <= 2, or two with |row| = 1.
+  //
+  // Base-conditioned folded gates (a CX whose control is a non-active qubit:
+  // term (single base bit, value) with vector e_a) flip selector a per tile;
+  // every combination of those base bits (<= 4) gets its own monomials under
+  // that base condition.
   bool conjugate(const Pre &p, const std::vector<int> &tile_of_slot, int K, Pre &out) const {
-    std::vector<std::pair<u32, int>> sels;  // (row mask, required parity)
+    struct Sel {
+      u32 row;
+      int w;      // required parity with all flip bits 0
+      u64 flips;  // base bits whose value XORs into the parity
+    };
+    std::vector<Sel> sels;
+    u64 U = 0;
     for (auto &sv : p.sel) {
       int a = tile_of_slot[sv.first];
       if (a < 0) continue;
+      Sel s{0, sv.second ^ (int)((c0 >> a) & 1), 0};
       for (auto &t : terms)
-        if ((std::get<2>(t) >> a) & 1) return false;
-      u32 row = 0;
+        if ((std::get<2>(t) >> a) & 1) {
+          const u64 bm = std::get<0>(t), bv = std::get<1>(t);
+          if (popc(bm) != 1) return false;
+          // [base & bm == bv] = base_bit ^ (bv == 0)
+          s.flips ^= bm;
+          if (bv == 0) s.w ^= 1;
+        }
       for (int b = 0; b < K; b++)
-        if ((col[b] >> a) & 1) row |= 1u << b;
-      sels.push_back({row, sv.second ^ (int)((c0 >> a) & 1)});
+        if ((col[b] >> a) & 1) s.row |= 1u << b;
+      U |= s.flips;
+      sels.push_back(s);
     }
+    if (popc(U) > 4) return false;
+    bool shape_ok = (sels.size() == 1 && popc((u64)sels[0].row) <= 2) ||
+                    (sels.size() == 2 && popc((u64)sels[0].row) == 1 &&
+                     popc((u64)sels[1].row) == 1 && sels[0].row != sels[1].row);
+    if (!shape_ok) return false;
     out = p;
     out.conj = true;
     out.mono.clear();
-    if (sels.size() == 1 && popc((u64)sels[0].first) <= 2) {
-      u32 r = sels[0].first;
-      int w = sels[0].second;
-      if (popc((u64)r) == 1) {
-        if (w) out.mono = {{r, 1}};
-        else out.mono = {{0u, 1}, {r, -1}};
+    std::vector<int> ub;
+    for (int b = 0; b < 64; b++)
+      if ((U >> b) & 1) ub.push_back(b);
+    for (int z = 0; z < (1 << ub.size()); z++) {
+      u64 bv = 0;
+      for (size_t i = 0; i < ub.size(); i++)
+        if ((z >> i) & 1) bv |= 1ull << ub[i];
+      auto wv = [&](const Sel &s) { return s.w ^ (popc(s.flips & bv) & 1); };
+      std::vector<std::pair<u32, int>> mm;
+      if (sels.size() == 1) {
+        u32 r = sels[0].row;
+        int w = wv(sels[0]);
+        if (popc((u64)r) == 1) {
+          if (w) mm = {{r, 1}};
+          else mm = {{0u, 1}, {r, -1}};
+        } else {
+          u32 a = r & (~r + 1), b = r ^ a;
+          if (w) mm = {{a, 1}, {b, 1}, {r, -2}};
+          else mm = {{0u, 1}, {a, -1}, {b, -1}, {r, 2}};
+        }
       } else {
-        u32 a = r & (~r + 1), b = r ^ a;
-        if (w) out.mono = {{a, 1}, {b, 1}, {r, -2}};
-        else out.mono = {{0u, 1}, {a, -1}, {b, -1}, {r, 2}};
+        u32 a = sels[0].row, b = sels[1].row;
+        int va = wv(sels[0]), vb = wv(sels[1]);
+        // [j_a == va][j_b == vb] expanded
+        if (va && vb) mm = {{a | b, 1}};
+        else if (va && !vb) mm = {{a, 1}, {a | b, -1}};
+        else if (!va && vb) mm = {{b, 1}, {a | b, -1}};
+        else mm = {{0u, 1}, {a, -1}, {b, -1}, {a | b, 1}};
       }
-    } else if (sels.size() == 2 && popc((u64)sels[0].first) == 1 && popc((u64)sels[1].first) == 1 &&
-               sels[0].first != sels[1].first) {
-      u32 a = sels[0].first, b = sels[1].first;
-      int va = sels[0].second, vb = sels[1].second;
-      // [j_a == va][j_b == vb] expanded
-      if (va && vb) out.mono = {{a | b, 1}};
-      else if (va && !vb) out.mono = {{a, 1}, {a | b, -1}};
-      else if (!va && vb) out.mono = {{b, 1}, {a | b, -1}};
-      else out.mono = {{0u, 1}, {a, -1}, {b, -1}, {a | b, 1}};
-    } else {
-      return false;
+      for (auto &x : mm) out.mono.push_back(Pre::Mono{x.first, x.second, U, bv});
     }
     out.tsel = 0;
-    for (auto &m : out.mono) out.tsel |= m.first;
+    for (auto &m : out.mono) out.tsel |= m.m;
     return true;
   }
   // tile bits the net folded map moves or reads: a later op may run before
@@ -837,9 +873,14 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                         cnd.base_mask |= 1ull << sv.first;
                         cnd.base_val |= (u64)sv.second << sv.first;
                       }
+                    // the monomial's own base condition (flips of folded
+                    // base-controlled gates); contradictory -> never applies
+                    if (((cnd.base_val ^ mo.bv) & cnd.base_mask & mo.bm) != 0) continue;
+                    cnd.base_mask |= mo.bm;
+                    cnd.base_val |= mo.bv;
                     int rr[2], nr = 0;
                     for (int b = 0; b < K_; b++)
-                      if ((mo.first >> b) & 1) {
+                      if ((mo.m >> b) & 1) {
                         if (reg_index[b] >= 0) rr[nr++] = reg_index[b];
                         else {
                           cnd.thr_mask |= (uint16_t)(1 << b);
@@ -847,7 +888,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                         }
                       }
                     const int slot = nr == 0 ? 0 : nr == 1 ? 1 + rr[0] : pair_slot(std::min(rr[0], rr[1]), std::max(rr[0], rr[1]));
-                    add(slot, cnd, std::pow(c, mo.second));
+                    add(slot, cnd, std::pow(c, mo.e));
                   }
                   continue;
                 }
