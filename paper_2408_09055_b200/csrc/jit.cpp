@@ -21,6 +21,8 @@
 #include <dlfcn.h>
 
 #include <atomic>
+#include <complex>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -344,27 +346,80 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       const ShmOp &op = ops[oi];
       const double *c = coef + op.coef;
       if (op.type == OP_DIAG) {
-        const int sel = kDiagSel[op.t0];
-        const int eb = (int)op.base_mask, ee = (int)op.base_val;
-        if (eb == ee) {
-          for (int e = 0; e < NE; e++)
-            if ((e & sel) == sel) emit_cmul_lit(o, e, c[0], c[1], f32, "      ");
-          continue;
+        // a run of consecutive factor-slot ops (one diagonal run): the
+        // per-element factor is the product of the slots covering it;
+        // unconditional slot factors are multiplied here (one literal per
+        // element), conditional ones once per thread at run time and shared
+        // between elements through partial products
+        int oj = oi;
+        while (oj < P.op_end && ops[oj].type == OP_DIAG) oj++;
+        struct Slot {
+          int sel;
+          std::complex<double> lit;
+          int rt;  // runtime factor index or -1
+        };
+        std::vector<Slot> slots;
+        int nrt = 0;
+        o << "      {\n";
+        for (int q = oi; q < oj; q++) {
+          const ShmOp &dq = ops[q];
+          const double *cq = coef + dq.coef;
+          const int eb = (int)dq.base_mask, ee = (int)dq.base_val;
+          Slot sl_{kDiagSel[dq.t0], {cq[0], cq[1]}, -1};
+          if (eb != ee) {
+            sl_.rt = nrt++;
+            o << "        T fr" << sl_.rt << "; { double fx = " << lit(cq[0], false) << ", fy = "
+              << lit(cq[1], false) << ";\n";
+            for (int i = eb; i < ee; i++) {
+              const DiagEnt &d = ents[i];
+              o << "          if (((jt & " << d.thr_mask << ") == " << d.thr_val << ")";
+              if (d.has_base)
+                o << " && ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val) << ")";
+              o << ") { const double nx = fx * " << lit(d.re, false) << " - fy * " << lit(d.im, false)
+                << "; fy = fx * " << lit(d.im, false) << " + fy * " << lit(d.re, false) << "; fx = nx; }\n";
+            }
+            o << "          fr" << sl_.rt << ".x = (R)fx; fr" << sl_.rt << ".y = (R)fy; }\n";
+            sl_.lit = 1.0;
+          }
+          slots.push_back(sl_);
         }
-        o << "      { double fx = " << lit(c[0], false) << ", fy = " << lit(c[1], false) << ";\n";
-        for (int i = eb; i < ee; i++) {
-          const DiagEnt &d = ents[i];
-          o << "        if (((jt & " << d.thr_mask << ") == " << d.thr_val << ")";
-          if (d.has_base) o << " && ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val) << ")";
-          o << ") { const double nx = fx * " << lit(d.re, false) << " - fy * " << lit(d.im, false)
-            << "; fy = fx * " << lit(d.im, false) << " + fy * " << lit(d.re, false) << "; fx = nx; }\n";
+        std::map<unsigned, std::string> prod;  // set of runtime factors -> variable
+        int ng = 0;
+        std::function<std::string(unsigned)> product = [&](unsigned set) -> std::string {
+          auto it = prod.find(set);
+          if (it != prod.end()) return it->second;
+          const int hi = 31 - __builtin_clz(set);
+          const unsigned rest = set & ~(1u << hi);
+          std::string nm;
+          if (!rest) {
+            nm = "fr" + std::to_string(hi);
+          } else {
+            const std::string a = product(rest);
+            nm = "g" + std::to_string(ng++);
+            o << "        T " << nm << "; " << nm << ".x = " << a << ".x * fr" << hi << ".x - " << a
+              << ".y * fr" << hi << ".y; " << nm << ".y = " << a << ".x * fr" << hi << ".y + " << a
+              << ".y * fr" << hi << ".x;\n";
+          }
+          prod[set] = nm;
+          return nm;
+        };
+        for (int e = 0; e < NE; e++) {
+          std::complex<double> L = 1.0;
+          unsigned rset = 0;
+          for (auto &q : slots)
+            if ((e & q.sel) == q.sel) {
+              if (q.rt >= 0) rset |= 1u << q.rt;
+              else L *= q.lit;
+            }
+          if (rset) {
+            const std::string g = product(rset);
+            o << "        { const T a = v[" << e << "]; v[" << e << "].x = " << g << ".x * a.x - " << g
+              << ".y * a.y; v[" << e << "].y = " << g << ".x * a.y + " << g << ".y * a.x; }\n";
+          }
+          emit_cmul_lit(o, e, L.real(), L.imag(), f32, "        ");
         }
-        o << "        T f; f.x = (R)fx; f.y = (R)fy;\n";
-        for (int e = 0; e < NE; e++)
-          if ((e & sel) == sel)
-            o << "        { const T a = v[" << e << "]; v[" << e << "].x = f.x * a.x - f.y * a.y; v[" << e
-              << "].y = f.x * a.y + f.y * a.x; }\n";
         o << "      }\n";
+        oi = oj - 1;
         continue;
       }
       const bool full = (op.flags & OPF_FULL) != 0;
