@@ -174,6 +174,9 @@ const char *atlas_last_error(void);
  *   "init"           1 = atlas_run starts from |0...0> [1]
  *   "timing"         1 = per-launch CUDA events (atlas_get_launches) [0]
  *   "shm_nbuf"       shared-memory tile buffers per CTA, 1..3 [1]
+ *   "shm_ctas"       plan-specialised kernels of 2^12-amplitude fp64 tiles:
+ *                    resident CTAs per SM, 2 (128 registers) or 3 (80
+ *                    registers, when their shared memory fits) [2]
  *   "shm_jit"        1 = each shared-memory launch runs a kernel generated
  *                    from its lowered op program and compiled with NVRTC for
  *                    sm_100a at the first atlas_run after a plan (cached per

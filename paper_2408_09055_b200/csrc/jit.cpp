@@ -171,7 +171,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   const ShmPhase *ph = C->phases.data() + sl.phase_off;
   const DiagEnt *ents = C->ents.data() + sl.ent_off;
   const PermTerm *terms = C->terms.data() + sl.term_off;
-  const int minb = (nbuf == 1 && (K - RB) >= 8 && (K - RB) <= 9 && (esz << K) <= 65536) ? 2 : 1;
+  int minb = (nbuf == 1 && (K - RB) >= 8 && (K - RB) <= 9 && (esz << K) <= 65536) ? 2 : 1;
 
   // distinct thread-index tables: jt per register mask, store offsets per
   // (register mask, permuted images)
@@ -207,7 +207,14 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   const size_t off_stab = off_jtab + (size_t)jmasks.size() * NT * 4;
   size_t off_btab = off_stab + (size_t)smaps.size() * NT * 2;
   off_btab = (off_btab + 15) & ~(size_t)15;
-  const size_t smem = off_btab + 4 * 256 * 8;
+  // tile-base deposit tables: one 256-entry table per byte of the tile index
+  int tbits = 0;
+  while ((1ull << tbits) < sl.ntiles) tbits++;
+  const int nbt = std::max(1, (tbits + 7) / 8);
+  const size_t smem = off_btab + (size_t)nbt * 256 * 8;
+  // option shm_ctas = 3: three resident CTAs per SM (register cap 80) when
+  // their shared memory fits the SM
+  if (minb == 2 && C->opt.shm_ctas >= 3 && 3 * (smem + 1024) <= 233472) minb = 3;
 
   std::ostringstream o;
   o << "// generated by jit.cpp: shared-memory kernel, K=" << K << " RB=" << RB
@@ -230,7 +237,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "  u64 *btab = reinterpret_cast<u64 *>(smraw + " << off_btab << ");\n";
   o << "  const int tid = threadIdx.x;\n";
   // tile-base deposit tables
-  o << "  for (int i = tid; i < 1024; i += " << NT << ") { const int c = i >> 8; u64 m = "
+  o << "  for (int i = tid; i < " << nbt * 256 << "; i += " << NT << ") { const int c = i >> 8; u64 m = "
     << u64lit(sl.nonactive) << "; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
     << "pdep64((u64)(i & 255), m); }\n";
   // per-thread tile indices of every distinct (register mask, lane order):
@@ -269,8 +276,9 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "\n  const int sw_tid = swz(tid);\n";
   o << "  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);\n";
   o << "  __syncthreads();\n";
-  o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255] | btab[256 + ((tile >> 8) & 255)] | "
-       "btab[512 + ((tile >> 16) & 255)] | btab[768 + ((tile >> 24) & 255)]; };\n";
+  o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255]";
+  for (int c = 1; c < nbt; c++) o << " | btab[" << 256 * c << " + ((tile >> " << 8 * c << ") & 255)]";
+  o << "; };\n";
   // per-register-element offsets (constant)
   std::vector<uint64_t> itoff(NE);
   for (int it = 0; it < NE; it++) {
