@@ -46,6 +46,8 @@ FULL_METRICS = [
 
 
 def launches(path):
+    """Per-kernel share table; the plan-specialised SHM kernels (one
+    atlas_shm_<hash> per launch of the plan) are also summed as one row."""
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -58,6 +60,10 @@ def launches(path):
         agg[k][0] += 1
         agg[k][1] += float(r[vi].replace(",", "")) * scale[r[ui]]
     tot = sum(v[1] for v in agg.values())
+    jit = [v for k, v in agg.items() if k.startswith("atlas_shm_")]
+    if jit:
+        agg["ALL atlas_shm_* (plan-specialised SHM kernels)"] = [sum(v[0] for v in jit),
+                                                                 sum(v[1] for v in jit)]
     out = ["| kernel | launches | total ms | avg ms | share |", "|---|---|---|---|---|"]
     for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         out.append(f"| `{k}` | {c} | {t:.2f} | {t / c:.4f} | {t / tot:.3f} |")
