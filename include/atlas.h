@@ -174,6 +174,11 @@ const char *atlas_last_error(void);
  *   "init"           1 = atlas_run starts from |0...0> [1]
  *   "timing"         1 = per-launch CUDA events (atlas_get_launches) [0]
  *   "shm_nbuf"       shared-memory tile buffers per CTA, 1..3 [1]
+ *   "shm_split_dense" complex 2x2 blocks in shared-memory kernels are applied
+ *                    as D1 R D2 (R real, D1/D2 diagonal, joined to the
+ *                    phase's diagonal runs) [1]
+ *   "shm_hoist_diag" diagonal ops move to the earliest diagonal run of their
+ *                    register phase they commute back to [1]
  *   "shm_ctas"       plan-specialised kernels of 2^12-amplitude fp64 tiles:
  *                    resident CTAs per SM, 2 (128 registers) or 3 (80
  *                    registers, when their shared memory fits) [2]

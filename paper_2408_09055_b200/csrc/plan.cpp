@@ -646,6 +646,56 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                     p.coef.push_back(blk[i].real());
                     p.coef.push_back(blk[i].imag());
                   }
+                // A complex 2x2 unitary block = D1 R D2 with R real and D1,
+                // D2 diagonal (Euler ZYZ form): the real block costs half the
+                // flops of the complex one, and the diagonal factors join the
+                // phase's diagonal runs (one multiply per element per run).
+                bool split = false;
+                cd d0, d1, e1;
+                double r[4];
+                if (!isx && C->opt.shm_split_dense) {
+                  bool cplx = false, tiny = false;
+                  for (int i = 0; i < 4; i++) {
+                    if (blk[i].imag() != 0.0) cplx = true;
+                    if (std::abs(blk[i]) < 1e-9) tiny = true;
+                  }
+                  if (cplx && !tiny) {
+                    r[0] = std::abs(blk[0]);
+                    r[2] = std::abs(blk[2]);
+                    d0 = blk[0] / r[0];
+                    d1 = blk[2] / r[2];
+                    r[1] = -std::abs(blk[1]);
+                    e1 = blk[1] / d0 / r[1];
+                    const cd r3 = blk[3] / (d1 * e1);
+                    r[3] = r3.real();
+                    double err = std::abs(r3.imag()) + std::abs(std::abs(e1) - 1.0);
+                    const cd rec[4] = {d0 * r[0], d0 * r[1] * e1, d1 * r[2], d1 * r[3] * e1};
+                    for (int i = 0; i < 4; i++) err += std::abs(rec[i] - blk[i]);
+                    split = err < 1e-13;
+                  }
+                }
+                if (split) {
+                  const int ts = mp.sigma[x.lq[tj[0]]];
+                  Pre pd2 = p, pd1a = p, pd1b = p;
+                  pd2.type = pd1a.type = pd1b.type = OP_PHASE;
+                  pd2.nt = pd1a.nt = pd1b.nt = 0;
+                  pd2.sel.push_back({ts, 1});
+                  pd2.coef = {e1.real(), e1.imag()};
+                  pd1a.coef = {d0.real(), d0.imag()};
+                  const cd q = d1 / d0;
+                  pd1b.sel.push_back({ts, 1});
+                  pd1b.coef = {q.real(), q.imag()};
+                  if (std::abs(e1 - cd(1)) > 1e-15) pre.push_back(pd2);
+                  p.coef.clear();
+                  for (int i = 0; i < 4; i++) {
+                    p.coef.push_back(r[i]);
+                    p.coef.push_back(0.0);
+                  }
+                  pre.push_back(p);
+                  if (std::abs(d0 - cd(1)) > 1e-15) pre.push_back(pd1a);
+                  if (std::abs(q - cd(1)) > 1e-15) pre.push_back(pd1b);
+                  continue;
+                }
               } else {
                 p.type = OP_DENSE2;
                 if (p.ttile[0] > p.ttile[1]) {  // canonical order t0 < t1
@@ -741,13 +791,43 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                   fresh();
                 }
               }
-              if (!cur->diag_open) {
-                cur->items.push_back({1, {}});
-                cur->diag_open = true;
-                cur->diag_bits = 0;
+              // hoist into the earliest diagonal run it can reach: it
+              // commutes with every dense op whose targets avoid its bits
+              // (all ops of a phase act on the pre-map tile index)
+              const u32 bits = pre[idx].tsel;
+              int cand = -1;
+              int at = (int)cur->items.size();
+              if (C->opt.shm_hoist_diag) {
+                for (int k2 = (int)cur->items.size() - 1; k2 >= 0; k2--) {
+                  auto &it = cur->items[k2];
+                  if (it.first == 1) {
+                    cand = k2;
+                    continue;
+                  }
+                  bool blocks = false;
+                  for (int o2 : it.second)
+                    if (pre[o2].tmask & bits) blocks = true;
+                  if (blocks) break;
+                  at = k2;
+                }
               }
-              cur->items.back().second.push_back(idx);
-              cur->diag_bits |= pre[idx].tsel;
+              const int last = (int)cur->items.size() - 1;
+              if (cand >= 0 && (cand != last || cur->diag_open)) {
+                cur->items[cand].second.push_back(idx);
+                if (cand == last) cur->diag_bits |= bits;
+                continue;
+              }
+              if (!C->opt.shm_hoist_diag || at >= (int)cur->items.size()) {
+                if (!cur->diag_open) {
+                  cur->items.push_back({1, {}});
+                  cur->diag_open = true;
+                  cur->diag_bits = 0;
+                }
+                cur->items.back().second.push_back(idx);
+                cur->diag_bits |= bits;
+              } else {
+                cur->items.insert(cur->items.begin() + at, {1, {idx}});
+              }
               continue;
             }
             if (cur->has_perm && ((p.tmask | p.tsel) & cur->touched(K_))) fresh();
