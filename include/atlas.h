@@ -164,7 +164,11 @@ const char *atlas_last_error(void);
  *   "prune_T"        Kernelize pruning threshold T [500];
  *                    <= 0 means no pruning
  *   "ls_qubits"      least-significant physical qubits forced into every
- *                    shared-memory kernel (P:L1964 footnote: 3) [5]
+ *                    shared-memory kernel (P:L1964 footnote: 3) [unset: the
+ *                    cost model's value (5), see "ls_auto"]
+ *   "ls_auto"        with ls_qubits unset and the built-in cost model, also
+ *                    plan with one forced qubit fewer and keep the plan of
+ *                    lower model cost (ties: the model's value) [1]
  *   "shm_qubits"     override q_max_shared of the cost model [model]
  *   "fusion_qubits"  override q_max_fusion of the cost model [model]
  *   "kinds"          bit 0 fusion, bit 1 shared-memory [3]

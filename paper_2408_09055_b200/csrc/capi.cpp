@@ -109,6 +109,31 @@ atlas_status atlas_plan(atlas_ctx *C, int s_max, double c) {
     need(s_max >= 1, ATLAS_E_INVALID, "s_max must be >= 1");
     need(c >= 0 && std::isfinite(c), ATLAS_E_INVALID, "c must be finite and >= 0");
     build_plan(C, s_max, c);
+    // ls_qubits unset with the built-in model: also plan with one forced
+    // least-significant qubit fewer (256-B runs stream as well as 512-B runs
+    // on B200 HBM3e, and a tile then spans one more high qubit) and keep the
+    // plan of lower model cost (ties: the model's setting)
+    if (C->opt.ls_qubits < 0 && C->opt.cost_model.empty() && C->opt.ls_auto &&
+        C->cm.ls_qubits > 3) {
+      auto total = [&]() {
+        int64_t t = 0;
+        for (auto &kp : C->kplans) t += kp.total;
+        return t;
+      };
+      const double us0 = C->plan_us;
+      const int64_t ca = total();
+      const int la = C->cm.ls_qubits;
+      C->opt.ls_qubits = la - 1;
+      build_plan(C, s_max, c);
+      double us = us0 + C->plan_us;
+      if (total() >= ca) {
+        C->opt.ls_qubits = la;
+        build_plan(C, s_max, c);
+        us += C->plan_us;
+      }
+      C->opt.ls_qubits = -1;
+      C->plan_us = us;
+    }
   })
 }
 
@@ -183,6 +208,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_direct_store") o.shm_direct_store = (int)v;
     else if (k == "shm_explicit_perm") o.shm_explicit_perm = (int)v;
     else if (k == "front") o.front = (int)v;
+    else if (k == "ls_auto") o.ls_auto = (int)v;
     else if (k == "shm_split_dense") o.shm_split_dense = (int)v;
     else if (k == "shm_hoist_diag") o.shm_hoist_diag = (int)v;
     else if (k == "shm_ctas") { need(v == 2 || v == 3, ATLAS_E_INVALID, "shm_ctas is 2 or 3"); o.shm_ctas = (int)v; C->jit_ready = false; replan = false; }

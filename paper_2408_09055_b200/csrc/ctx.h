@@ -52,6 +52,7 @@ struct Options {
   int kernelizer = 0;
   int prune_T = 500;
   int ls_qubits = 5;
+  int ls_auto = 1;           // ls_qubits unset: also try one fewer, keep the cheaper plan
   int shm_qubits = -1;
   int fusion_qubits = -1;
   int kinds = 3;
