@@ -223,3 +223,37 @@ def test_shm_interpreter_variants(fam, opt):
     c = C.random_circuit(13, 150, 78) if fam == "random" else C.make(fam, 13)
     psi, _ = run(c, shm_jit=0, **opt)
     check(psi, O.simulate(c))
+
+
+# ------------------------------------------------------------- n = 33
+# BASELINE config 4 at N = 1: 2^33 fp64 amplitudes = 128 GiB in one B200's
+# HBM (the largest single-GPU size), checked against closed forms.
+
+def test_qft_n33_basis_state():
+    """qft n=33 from |x>: amp(y) = 2^{-n/2} exp(2 pi i rev(x) y / 2^n) (P4),
+    at sampled y (64-bit indexing, 2^21 tiles)."""
+    n = 33
+    x = 0x15A3C1F7 & ((1 << n) - 1)
+    c = C.prepend_basis(C.qft(n), x)
+    rev = int(format(x, f"0{n}b")[::-1], 2)
+    with A.Simulator(n, 0, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.run()
+        idx = _sample_idx(n, 64, 5)
+        got = _amps(s, idx)
+    want = np.array([np.exp(2j * np.pi * ((rev * y) % (1 << n)) / (1 << n)) for y in idx]) * 2 ** (-n / 2)
+    assert np.abs(got - want).max() <= 1e-10
+
+
+def test_ghz_n33():
+    n = 33
+    c = C.ghz(n)
+    with A.Simulator(n, 0, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.run()
+        idx = _sample_idx(n, 64, 6)
+        got = _amps(s, idx)
+    want = np.array([2 ** -0.5 if i in (0, (1 << n) - 1) else 0.0 for i in idx])
+    assert np.abs(got - want).max() <= 1e-10
