@@ -176,6 +176,9 @@ const char *atlas_last_error(void);
  *   "attach"         Kernelize single-qubit attachment [1]
  *   "virtual_world"  1 = all ranks on this GPU (see atlas_create) [0]
  *   "init"           1 = atlas_run starts from |0...0> [1]
+ *   "init_fuse"      1 = when the first launch is a plan-specialised
+ *                    shared-memory kernel, it synthesises |0...0> in
+ *                    registers instead of reading a memset shard [1]
  *   "timing"         1 = per-launch CUDA events (atlas_get_launches) [0]
  *   "shm_nbuf"       shared-memory tile buffers per CTA, 1..3 [1]
  *   "shm_split_dense" complex 2x2 blocks in shared-memory kernels are applied

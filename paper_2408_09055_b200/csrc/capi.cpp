@@ -208,6 +208,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_direct_store") o.shm_direct_store = (int)v;
     else if (k == "shm_explicit_perm") o.shm_explicit_perm = (int)v;
     else if (k == "front") o.front = (int)v;
+    else if (k == "init_fuse") { o.init_fuse = (int)v; replan = false; }
     else if (k == "ls_auto") o.ls_auto = (int)v;
     else if (k == "shm_split_dense") o.shm_split_dense = (int)v;
     else if (k == "shm_hoist_diag") o.shm_hoist_diag = (int)v;

@@ -60,6 +60,7 @@ struct Options {
   int attach = 1;
   int virtual_world = 0;
   int init = 1;
+  int init_fuse = 1;         // |0...0> synthesised by the first SHM kernel (no memset pass)
   int timing = 0;
   int device = -1;
   long stage_budget = 2000000;

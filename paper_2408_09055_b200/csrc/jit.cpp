@@ -85,6 +85,7 @@ struct JitEntry {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
   int smem = 0, nt = 0, attr_set = 0;
+  bool zero_ok = false;
 };
 std::mutex g_cache_mu;
 std::unordered_map<std::string, JitEntry *> g_cache;  // source -> compiled kernel
@@ -222,6 +223,10 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "typedef unsigned long long u64; typedef unsigned int u32; typedef unsigned short u16;\n";
   o << (f32 ? "typedef float R; typedef float2 T;\n" : "typedef double R; typedef double2 T;\n");
   o << "#define SMEM_BYTES " << smem << "\n";
+  // zmode (early pipeline only): 1 = the input is all zeros, 2 = the input
+  // is |0...0> on this rank (atlas_run's initial state): the first tile
+  // load is synthesised in registers and nothing is read from HBM
+  o << "#define ZERO_OK " << (nbuf == 1 ? 1 : 0) << "\n";
   o << "__device__ __forceinline__ int swz(int j) { return "
     << (f32 ? "j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15)"
             : "j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7)")
@@ -229,7 +234,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "__device__ __forceinline__ u64 pdep64(u64 v, u64 mask) { u64 r = 0; while (mask) { u64 lo = "
        "mask & (~mask + 1); if (v & 1) r |= lo; v >>= 1; mask ^= lo; } return r; }\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
-    << "(T *__restrict__ st) {\n";
+    << "(T *__restrict__ st, int zmode) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
@@ -314,9 +319,9 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   const bool early = nbuf == 1;
   const std::string NTL = u64lit(sl.ntiles);
   const std::string next_issue =
-      "{ const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
+      "if (!zmode) { const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
   if (early) {
-    o << "  issue_load(0, tile_base(tile));\n";
+    o << "  if (!zmode) issue_load(0, tile_base(tile));\n";
   } else {
     for (int k = 0; k < nbuf - 1; k++)
       o << "  { const u64 t = tile + " << k << "ull * G; if (t < " << NTL
@@ -347,7 +352,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       int a = 0;
       for (int i = 0; i < RB; i++)
         if ((e >> i) & 1) a ^= sr[i];
+      if (early && p == 0 && e == 0) o << "      if (zmode) {\n";
+      if (early && p == 0 && e == 0) {
+        for (int e2 = 0; e2 < NE; e2++) o << "        v[" << e2 << "].x = 0; v[" << e2 << "].y = 0;\n";
+        o << "        if (zmode == 2 && tile == 0 && jt == 0) v[0].x = 1;\n      } else {\n";
+      }
       o << "      v[" << e << "] = tb[sj ^ " << a << "];\n";
+      if (early && p == 0 && e == NE - 1) o << "      }\n";
     }
     if (early && ld && p == last) o << "      __syncthreads();\n      " << next_issue << "\n";
     for (int oi = P.op_begin; oi < P.op_end; oi++) {
@@ -546,6 +557,10 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   return o.str();
 }
 
+static bool shm_jit_zero_ok_src(const std::string &src) {
+  return strstr(src.c_str(), "#define ZERO_OK 1") != nullptr;
+}
+
 size_t shm_jit_smem(const std::string &src) {
   const char *p = strstr(src.c_str(), "#define SMEM_BYTES ");
   return p ? (size_t)strtoull(p + 19, nullptr, 10) : 0;
@@ -622,6 +637,7 @@ static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &s
     e = cudaLibraryGetKernel(&E->kern, E->lib, names[i].c_str());
     if (e != cudaSuccess) fail(ATLAS_E_CUDA, "cudaLibraryGetKernel: %s", cudaGetErrorString(e));
     E->smem = (int)shm_jit_smem(srcs[i]);
+    E->zero_ok = shm_jit_zero_ok_src(srcs[i]);
     g_cache[srcs[i]] = E;
     out[i] = E;
   }
@@ -655,7 +671,9 @@ void shm_jit_prepare(atlas_ctx *C) {
 
 static int g_nsms = 0;
 
-cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s) {
+bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->zero_ok; }
+
+cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s, int zmode) {
   JitEntry *E = (JitEntry *)jit;
   const int NT = 1 << (sl.K - sl.RB);
   if (E->attr_set < E->smem) {
@@ -676,7 +694,7 @@ cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_
   }
   uint64_t grid = (uint64_t)g_nsms * E->nt;
   if (grid > sl.ntiles) grid = sl.ntiles;
-  void *args[] = {&st};
+  void *args[] = {&st, &zmode};
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);
 }

@@ -31,7 +31,8 @@ cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const in
 cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
 void shm_jit_prepare(atlas_ctx *C);
-cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s);
+cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s, int zmode);
+bool shm_jit_zero_ok(const void *jit);
 
 #define CK(x)                                                                              \
   do {                                                                                     \
@@ -281,10 +282,20 @@ void run(atlas_ctx *C) {
   auto mark_end = [&]() {
     if (timing) CK(cudaEventRecord(ev_at(nev++), C->stream));
   };
-  // init |0...0>: logical 0 -> physical 0 (no flips at stage 0) on rank 0
+  // init |0...0>: logical 0 -> physical 0 (no flips at stage 0) on rank 0.
+  // When the first launch of stage 0 is a plan-specialised shared-memory
+  // kernel it synthesises that input itself (zmode) instead of reading a
+  // memset shard: one write-only pass fewer.
+  std::vector<int> zmode(C->nslots, 0);
   for (int s = 0; s < C->nslots; s++) {
     if (!C->opt.init && C->state_set) continue;
     C->cur[s] = 0;
+    const auto &P = C->prog[s];
+    if (C->opt.init_fuse && !P.empty() && P[0].stage == 0 && P[0].type == L_SHM &&
+        shm_jit_zero_ok(P[0].jit)) {
+      zmode[s] = slot_rank(C, s) == 0 ? 2 : 1;
+      continue;
+    }
     mark(L_INIT, (int64_t)shard_bytes(C));
     CK(launch_init(dt, cur_buf(C, s), C->L, slot_rank(C, s) == 0, C->stream));
     mark_end();
@@ -318,12 +329,14 @@ void run(atlas_ctx *C) {
       while (pc[s] < P.size() && P[pc[s]].stage == k) {
         const Launch &ln = P[pc[s]++];
         void *st = cur_buf(C, s);
-        mark(ln.type, ln.bytes);
+        // a launch that synthesises |0...0> only writes the shard
+        const int zm = (k == 0 && pc[s] == 1 && ln.type == L_SHM && ln.jit) ? zmode[s] : 0;
+        mark(ln.type, zm ? ln.bytes / 2 : ln.bytes);
         switch (ln.type) {
           case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
           case L_SHM:
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, ln.sl, C->stream));
+              CK(launch_shm_jit(ln.jit, st, ln.sl, C->stream, zm));
               break;
             }
             CK(launch_shm(dt, st, ln.sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
