@@ -186,6 +186,10 @@ const char *atlas_last_error(void);
  *                    phase's diagonal runs) [1]
  *   "shm_hoist_diag" diagonal ops move to the earliest diagonal run of their
  *                    register phase they commute back to [1]
+ *   "shm_pipe"       plan-specialised kernels with one tile buffer: one CTA
+ *                    per SM of two thread groups sharing a ring of three
+ *                    tile buffers (loads complete on mbarriers); measured
+ *                    slower than 2 CTAs of one buffer on n=28 [0]
  *   "shm_ctas"       plan-specialised kernels of 2^12-amplitude fp64 tiles:
  *                    resident CTAs per SM, 2 (128 registers) or 3 (80
  *                    registers, when their shared memory fits) [2]

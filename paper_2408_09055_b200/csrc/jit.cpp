@@ -84,7 +84,7 @@ void nvrtc_load() {
 struct JitEntry {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
-  int smem = 0, nt = 0, attr_set = 0;
+  int smem = 0, nt = 0, attr_set = 0, threads = 0;
   bool zero_ok = false;
 };
 std::mutex g_cache_mu;
@@ -204,15 +204,28 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       sslot[p] = ss;
     }
   }
-  const size_t off_jtab = (size_t)nbuf * TILE * esz;
-  const size_t off_stab = off_jtab + (size_t)jmasks.size() * NT * 4;
-  size_t off_btab = off_stab + (size_t)smaps.size() * NT * 2;
-  off_btab = (off_btab + 15) & ~(size_t)15;
   // tile-base deposit tables: one 256-entry table per byte of the tile index
   int tbits = 0;
   while ((1ull << tbits) < sl.ntiles) tbits++;
   const int nbt = std::max(1, (tbits + 7) / 8);
-  const size_t smem = off_btab + (size_t)nbt * 256 * 8;
+  auto layout = [&](int ntile_bufs, size_t &oj, size_t &os, size_t &ob, size_t &om) {
+    oj = (size_t)ntile_bufs * TILE * esz;
+    os = oj + (size_t)jmasks.size() * NT * 4;
+    ob = (os + (size_t)smaps.size() * NT * 2 + 15) & ~(size_t)15;
+    om = ob + (size_t)nbt * 256 * 8;
+    return om + 3 * 8;
+  };
+  size_t off_jtab, off_stab, off_btab, off_mbar;
+  // pipe: one CTA of two thread groups (each a full tile's worth of
+  // threads, named barriers) sharing a ring of three tile buffers: a tile's
+  // load is issued into the buffer the other group just finished with, so up
+  // to two loads are in flight while both groups compute; completion is
+  // tracked by cp.async -> mbarrier arrivals
+  bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 1024 &&
+              layout(3, off_jtab, off_stab, off_btab, off_mbar) + 1024 <= 233472;
+  const size_t smem = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar);
+  const int BT = pipe ? 2 * NT : NT;  // threads per CTA
+  if (pipe) minb = 1;
   // option shm_ctas = 3: three resident CTAs per SM (register cap 80) when
   // their shared memory fits the SM
   if (minb == 2 && C->opt.shm_ctas >= 3 && 3 * (smem + 1024) <= 233472) minb = 3;
@@ -233,16 +246,31 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     << "; }\n";
   o << "__device__ __forceinline__ u64 pdep64(u64 v, u64 mask) { u64 r = 0; while (mask) { u64 lo = "
        "mask & (~mask + 1); if (v & 1) r |= lo; v >>= 1; mask ^= lo; } return r; }\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
+  o << "#define BLOCK_THREADS " << BT << "\n";
+  if (pipe) {
+    o << "__device__ __forceinline__ void gsync(int g) { asm volatile(\"bar.sync %0, " << NT
+      << ";\" :: \"r\"(1 + g) : \"memory\"); }\n";
+    o << "__device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) { unsigned ok = 0; do { "
+         "asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 "
+         "%0, 1, 0, p; }\" : \"=r\"(ok) : \"r\"(a), \"r\"(par) : \"memory\"); } while (!ok); }\n";
+  }
+  o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
     << "(T *__restrict__ st, int zmode) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
   o << "  u16 *stab = reinterpret_cast<u16 *>(smraw + " << off_stab << ");\n";
   o << "  u64 *btab = reinterpret_cast<u64 *>(smraw + " << off_btab << ");\n";
-  o << "  const int tid = threadIdx.x;\n";
+  if (pipe) {
+    o << "  const int tid = threadIdx.x & " << NT - 1 << ", grp = threadIdx.x / " << NT << ";\n";
+    o << "  const unsigned mbar0 = (unsigned)__cvta_generic_to_shared(smraw + " << off_mbar << ");\n";
+    o << "  if (threadIdx.x == 0) for (int i = 0; i < 3; i++) asm volatile(\"mbarrier.init.shared::cta.b64 "
+         "[%0], %1;\" :: \"r\"(mbar0 + 8 * i), \"r\"(" << NT << ") : \"memory\");\n";
+  } else {
+    o << "  const int tid = threadIdx.x;\n";
+  }
   // tile-base deposit tables
-  o << "  for (int i = tid; i < " << nbt * 256 << "; i += " << NT << ") { const int c = i >> 8; u64 m = "
+  o << "  for (int i = threadIdx.x; i < " << nbt * 256 << "; i += " << BT << ") { const int c = i >> 8; u64 m = "
     << u64lit(sl.nonactive) << "; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
     << "pdep64((u64)(i & 255), m); }\n";
   // per-thread tile indices of every distinct (register mask, lane order):
@@ -262,6 +290,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       if (!((used >> b) & 1)) ord.push_back(b);
     return ord;
   };
+  if (pipe) o << "  if (grp == 0) {\n";
   for (size_t js = 0; js < jmasks.size(); js++) {
     o << "  { int jt = 0;";
     const std::vector<int> ord = thread_order(jmasks[js]);
@@ -275,6 +304,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       o << " if ((tid >> " << t << ") & 1) sa ^= " << smaps[ss].second[ord[t]] << "u;";
     o << " stab[" << ss * NT << " + tid] = (u16)sa; }\n";
   }
+  if (pipe) o << "  }\n";
   // this thread's HBM offset inside a tile
   o << "  u64 off_t = 0;";
   for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) off_t |= " << u64lit(1ull << sl.act[i]) << ";";
@@ -299,7 +329,15 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     if (!f32) o << "asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
     else o << "asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
   }
-  o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n  };\n";
+  if (pipe)
+    o << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(mbar0 + 8 * bsel) : \"memory\");\n  };\n";
+  else
+    o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n  };\n";
+  // pipe, zero mode: the ring protocol without data (plain arrivals)
+  if (pipe)
+    o << "  auto issue = [&](int bsel, u64 base) { if (!zmode) issue_load(bsel, base); else asm volatile("
+         "\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mbar0 + 8 * bsel) : \"memory\"); };\n";
+  const std::string GS = pipe ? "gsync(grp);" : "__syncthreads();";
 
   const int last = sl.nphase - 1;
   const bool ld = sl.last_direct != 0;
@@ -309,8 +347,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       if (sl.lcol[b]) o << " if ((jtl >> " << b << ") & 1) gthr ^= " << u64lit(sl.lcol[b]) << ";";
     o << " }\n";
   }
-  o << "  u64 tile = blockIdx.x;\n  if (tile >= " << u64lit(sl.ntiles) << ") return;\n";
-  o << "  const u64 G = gridDim.x;\n";
+  if (pipe) {
+    o << "  const u64 G = gridDim.x;\n";
+    o << "  if ((u64)blockIdx.x >= " << u64lit(sl.ntiles) << ") return;\n";
+  } else {
+    o << "  u64 tile = blockIdx.x;\n  if (tile >= " << u64lit(sl.ntiles) << ") return;\n";
+    o << "  const u64 G = gridDim.x;\n";
+  }
   // early = one tile buffer: the next tile's load is issued as soon as every
   // thread has read the current tile out of shared memory for the last time
   // (the last phase's gather, or the copy-out), so it overlaps the last
@@ -319,18 +362,33 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   const bool early = nbuf == 1;
   const std::string NTL = u64lit(sl.ntiles);
   const std::string next_issue =
-      "if (!zmode) { const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
-  if (early) {
+      pipe ? "{ const u64 nx = blockIdx.x + (i + 3) * G; if (nx < " + NTL + ") issue(b, tile_base(nx)); }"
+           : "if (!zmode) { const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
+  if (pipe) {
+    // tiles i = 0, 1, 2 of this CTA's sequence into buffers 0, 1, 2, each
+    // issued by the group that will process it (i & 1)
+    o << "  for (int i = grp; i < 3; i += 2) { const u64 t = blockIdx.x + (u64)i * G; if (t < " << NTL
+      << ") issue(i, tile_base(t)); }\n";
+  } else if (early) {
     o << "  if (!zmode) issue_load(0, tile_base(tile));\n";
   } else {
     for (int k = 0; k < nbuf - 1; k++)
       o << "  { const u64 t = tile + " << k << "ull * G; if (t < " << NTL
         << ") issue_load(" << k << ", tile_base(t)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); }\n";
   }
+  if (pipe) {
+    o << "  for (u64 i = grp;; i += 2) {\n";
+    o << "    const u64 tile = blockIdx.x + i * G;\n    if (tile >= " << NTL << ") break;\n";
+    o << "    const u64 base = tile_base(tile);\n";
+    o << "    const int b = (int)(i % 3);\n";
+    o << "    mbar_wait(mbar0 + 8 * b, (unsigned)((i / 3) & 1));\n";
+  } else {
   o << "  int b = 0;\n";
   o << "  for (; tile < " << NTL << "; tile += G) {\n";
   o << "    const u64 base = tile_base(tile);\n";
-  if (early) {
+  }
+  if (pipe) {
+  } else if (early) {
     o << "    asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
   } else {
     o << "    { const u64 far = tile + " << (nbuf - 1) << "ull * G; const int fb = (b + " << (nbuf - 1)
@@ -338,7 +396,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       << ") issue_load(fb, tile_base(far)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");"
       << " asm volatile(\"cp.async.wait_group " << (nbuf - 1) << ";\\n\" ::: \"memory\"); }\n";
   }
-  o << "    __syncthreads();\n";
+  if (!pipe) o << "    __syncthreads();\n";
   o << "    T *tb = buf + b * " << TILE << ";\n";
   o << "    T v[" << NE << "];\n";
   for (int p = 0; p < sl.nphase; p++) {
@@ -360,7 +418,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       o << "      v[" << e << "] = tb[sj ^ " << a << "];\n";
       if (early && p == 0 && e == NE - 1) o << "      }\n";
     }
-    if (early && ld && p == last) o << "      __syncthreads();\n      " << next_issue << "\n";
+    if (early && ld && p == last) o << "      " << GS << "\n      " << next_issue << "\n";
     for (int oi = P.op_begin; oi < P.op_end; oi++) {
       const ShmOp &op = ops[oi];
       const double *c = coef + op.coef;
@@ -522,7 +580,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
         o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
           << ") cb ^= " << terms[i].vec_swz << "u;\n";
       o << "      const int s0 = (int)(stab[" << sslot[p] * NT << " + tid] ^ cb);\n";
-      o << "      __syncthreads();\n";
+      o << "      " << GS << "\n";
       for (int e = 0; e < NE; e++) {
         int a = 0;
         for (int i = 0; i < RB; i++)
@@ -537,13 +595,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
         o << "      tb[sj ^ " << a << "] = v[" << e << "];\n";
       }
     }
-    o << "      __syncthreads();\n    }\n";
+    o << "      " << GS << "\n    }\n";
   }
   if (!ld) {
     o << "    { T *g = st + base + off_t;\n";
     if (early) {
       for (int it = 0; it < NE; it++) o << "      v[" << it << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
-      o << "      __syncthreads();\n      " << next_issue << "\n";
+      o << "      " << GS << "\n      " << next_issue << "\n";
       for (int it = 0; it < NE; it++) o << "      g[" << u64lit(itoff[it]) << "] = v[" << it << "];\n";
     } else {
       for (int it = 0; it < NE; it++)
@@ -552,7 +610,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     o << "    }\n";
   }
   if (!early) o << "    __syncthreads();\n";
-  o << "    b = (b + 1) % " << nbuf << ";\n";
+  if (!pipe) o << "    b = (b + 1) % " << nbuf << ";\n";
   o << "  }\n}\n";
   return o.str();
 }
@@ -638,6 +696,10 @@ static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &s
     if (e != cudaSuccess) fail(ATLAS_E_CUDA, "cudaLibraryGetKernel: %s", cudaGetErrorString(e));
     E->smem = (int)shm_jit_smem(srcs[i]);
     E->zero_ok = shm_jit_zero_ok_src(srcs[i]);
+    {
+      const char *p = strstr(srcs[i].c_str(), "#define BLOCK_THREADS ");
+      E->threads = p ? atoi(p + 22) : 0;
+    }
     g_cache[srcs[i]] = E;
     out[i] = E;
   }
@@ -675,7 +737,7 @@ bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->z
 
 cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s, int zmode) {
   JitEntry *E = (JitEntry *)jit;
-  const int NT = 1 << (sl.K - sl.RB);
+  const int NT = E->threads > 0 ? E->threads : 1 << (sl.K - sl.RB);
   if (E->attr_set < E->smem) {
     cudaError_t e = cudaFuncSetAttribute((const void *)E->kern,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, E->smem);

@@ -220,7 +220,12 @@ def test_front_packing_cx_block_windows():
     from workloads.circuits import Gate, Circuit
     n = 20
     c = Circuit(n, [Gate("CX", (i, j)) for i in range(n) for j in range(i + 1, n)])
-    pj = product_plan(c, 1, kernelizer=3, kinds=2)
+    pj = product_plan(c, 1, kernelizer=3, kinds=2, ls_qubits=5)
     assert len(pj["stages"][0]["kernels"]) == 3
-    pk = product_plan(c, 1, kernelizer=0, kinds=2)
+    pk = product_plan(c, 1, kernelizer=0, kinds=2, ls_qubits=5)
     assert len(pk["stages"][0]["kernels"]) == 3
+    # ls_auto (ls_qubits unset): 4 forced LSB qubits -> windows of 8 targets
+    # (4..11, 12..19) -> 2 kernels; the model keeps the cheaper plan
+    pa = product_plan(c, 1, kernelizer=3, kinds=2)
+    assert pa["ls_qubits"] in (4, 5)
+    assert len(pa["stages"][0]["kernels"]) <= 3
