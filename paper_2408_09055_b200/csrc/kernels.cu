@@ -749,7 +749,7 @@ static cudaError_t launch_shm_t(void *st, const ShmLaunch &sl, const ShmOp *ops,
         return launch_shm_k<R, 12, 4, 3>(st, sl, ops, coef, ph, ents, terms, s);
       return sl.nbuf == 1 ? launch_shm_k<R, 12, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
                           : launch_shm_k<R, 12, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
-    case 13: return F64 ? launch_shm_k<R, 13, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
+    case 13: return (F64 || sl.nbuf == 1) ? launch_shm_k<R, 13, 4, 1>(st, sl, ops, coef, ph, ents, terms, s)
                         : launch_shm_k<R, 13, 4, 2>(st, sl, ops, coef, ph, ents, terms, s);
   }
   return cudaErrorInvalidValue;
@@ -768,7 +768,7 @@ int shm_nbuf_effective(int dtype, const ShmLaunch &sl) {
     if (sl.nbuf == 3 && shm_smem_layout(esz << 12, 3, sl, 256, 16).total <= 232448) return 3;
     return sl.nbuf == 1 ? 1 : 2;
   }
-  return F64 ? 1 : 2;
+  return (F64 || sl.nbuf == 1) ? 1 : 2;
 }
 
 cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *ops,
