@@ -29,7 +29,11 @@ N = 28
 
 
 def launch_ms(gates, dtype, reps, **opt):
-    s = A.Simulator(N, dtype, 1, 0, kernelizer=1, **opt)
+    # init_fuse=0: the measured launch must read and write the shard (the
+    # fused |0> initialisation would make the first kernel write-only);
+    # ls_qubits fixed so the calibration circuits keep their one-kernel plans
+    opt.setdefault("ls_qubits", 5)
+    s = A.Simulator(N, dtype, 1, 0, kernelizer=1, init_fuse=0, **opt)
     s.load_circuit(gates)
     s.plan(4, 3.0)
     pj = s.plan_json()
