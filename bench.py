@@ -46,7 +46,7 @@ FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--workload", default="su2random_n28")
     p.add_argument("--impl", default="atlas", choices=["atlas", "reference"])
@@ -87,13 +87,27 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a moment to start: wait for its first sample
+            # so the timed region that follows is covered
+            t_end = time.time() + 5.0
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+        self.t0 = time.time()
+        self.t1 = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, start: bool):
+        """Bracket the timed region (samples outside it are not reported)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -105,7 +119,12 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        for ln in self.lines:
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        # a 100 ms sampler: keep the samples taken inside the timed region
+        # (plus one period of slack at the end)
+        for t, ln in self.lines:
+            if t < self.t0 or t > t1 + 0.1:
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -249,12 +268,14 @@ def run_atlas(args):
     with ClockSampler(dev) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
+        clk.mark(True)
         ev0.record(stream)
         for _ in range(args.steps):
             sim.run()
             launches.extend(sim.launches())
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
     barrier()
     ms = ev0.elapsed_time(ev1)
     if dist is not None:
