@@ -445,15 +445,17 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
           Slot sl_{kDiagSel[dq.t0], {cq[0], cq[1]}, -1};
           if (eb != ee) {
             sl_.rt = nrt++;
-            o << "        T fr" << sl_.rt << "; { double fx = " << lit(cq[0], false) << ", fy = "
-              << lit(cq[1], false) << ";\n";
+            // accumulated in R (fp32 runs: the product of a few unit phases
+            // stays far inside BJ's 1e-4; keeps the 64-register budget)
+            o << "        T fr" << sl_.rt << "; { R fx = " << lit(cq[0], f32) << ", fy = "
+              << lit(cq[1], f32) << ";\n";
             for (int i = eb; i < ee; i++) {
               const DiagEnt &d = ents[i];
               o << "          if (((jt & " << d.thr_mask << ") == " << d.thr_val << ")";
               if (d.has_base)
                 o << " && ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val) << ")";
-              o << ") { const double nx = fx * " << lit(d.re, false) << " - fy * " << lit(d.im, false)
-                << "; fy = fx * " << lit(d.im, false) << " + fy * " << lit(d.re, false) << "; fx = nx; }\n";
+              o << ") { const R nx = fx * " << lit(d.re, f32) << " - fy * " << lit(d.im, f32)
+                << "; fy = fx * " << lit(d.im, f32) << " + fy * " << lit(d.re, f32) << "; fx = nx; }\n";
             }
             o << "          fr" << sl_.rt << ".x = (R)fx; fr" << sl_.rt << ".y = (R)fy; }\n";
             sl_.lit = 1.0;
