@@ -654,12 +654,16 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                 cd d0, d1, e1;
                 double r[4];
                 if (!isx && C->opt.shm_split_dense) {
-                  bool cplx = false, tiny = false;
+                  // worth it only when the complex block has more nonzero
+                  // real/imaginary parts than the 4 of a real block (RX's
+                  // entries are each real or imaginary: no gain)
+                  bool tiny = false;
+                  int parts = 0;
                   for (int i = 0; i < 4; i++) {
-                    if (blk[i].imag() != 0.0) cplx = true;
+                    parts += (blk[i].real() != 0.0) + (blk[i].imag() != 0.0);
                     if (std::abs(blk[i]) < 1e-9) tiny = true;
                   }
-                  if (cplx && !tiny) {
+                  if (parts > 4 && !tiny) {
                     r[0] = std::abs(blk[0]);
                     r[2] = std::abs(blk[2]);
                     d0 = blk[0] / r[0];
