@@ -208,12 +208,32 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   int tbits = 0;
   while ((1ull << tbits) < sl.ntiles) tbits++;
   const int nbt = std::max(1, (tbits + 7) / 8);
+  // base-only conditional factors of diagonal slots (conditions on
+  // non-active qubits only: uniform over a tile) are evaluated once per tile
+  // by one designated thread per slot into a double-buffered SMEM table
+  // instead of by every thread
+  std::map<int, int> bslot;  // op index -> base-factor slot
+  if (!C->opt.shm_pipe)
+    for (int q = 0; q < sl.nops; q++) {
+      const ShmOp &dq = ops[q];
+      if (dq.type != OP_DIAG) continue;
+      bool any = false;
+      for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++)
+        if (ents[i].thr_mask == 0 && ents[i].has_base) any = true;
+      if (any) {
+        const int k = (int)bslot.size();
+        bslot[q] = k;
+      }
+    }
+  const int NB = (int)bslot.size();
+  size_t off_bfac = 0;
   auto layout = [&](int ntile_bufs, size_t &oj, size_t &os, size_t &ob, size_t &om) {
     oj = (size_t)ntile_bufs * TILE * esz;
     os = oj + (size_t)jmasks.size() * NT * 4;
     ob = (os + (size_t)smaps.size() * NT * 2 + 15) & ~(size_t)15;
     om = ob + (size_t)nbt * 256 * 8;
-    return om + 3 * 8;
+    off_bfac = (om + 3 * 8 + 15) & ~(size_t)15;
+    return off_bfac + (size_t)2 * NB * esz;
   };
   size_t off_jtab, off_stab, off_btab, off_mbar;
   // pipe: one CTA of two thread groups (each a full tile's worth of
@@ -261,6 +281,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
   o << "  u16 *stab = reinterpret_cast<u16 *>(smraw + " << off_stab << ");\n";
   o << "  u64 *btab = reinterpret_cast<u64 *>(smraw + " << off_btab << ");\n";
+  if (NB) o << "  T *bfac = reinterpret_cast<T *>(smraw + " << off_bfac << ");\n  int itp = 0;\n";
   if (pipe) {
     o << "  const int tid = threadIdx.x & " << NT - 1 << ", grp = threadIdx.x / " << NT << ";\n";
     o << "  const unsigned mbar0 = (unsigned)__cvta_generic_to_shared(smraw + " << off_mbar << ");\n";
@@ -386,6 +407,22 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "  int b = 0;\n";
   o << "  for (; tile < " << NTL << "; tile += G) {\n";
   o << "    const u64 base = tile_base(tile);\n";
+  const int nwarps = BT / 32;
+  for (auto &kv : bslot) {
+    const int bk = kv.second;
+    const ShmOp &dq = ops[kv.first];
+    const int desig = (bk % nwarps) * 32 + (bk / nwarps) % 32;
+    o << "    if (threadIdx.x == " << desig << ") { R fx = 1, fy = 0;\n";
+    for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++) {
+      const DiagEnt &d = ents[i];
+      if (!(d.thr_mask == 0 && d.has_base)) continue;
+      o << "      if ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val)
+        << ") { const R nx = fx * " << lit(d.re, f32) << " - fy * " << lit(d.im, f32) << "; fy = fx * "
+        << lit(d.im, f32) << " + fy * " << lit(d.re, f32) << "; fx = nx; }\n";
+    }
+    o << "      bfac[itp * " << NB << " + " << bk << "].x = fx; bfac[itp * " << NB << " + " << bk
+      << "].y = fy; }\n";
+  }
   }
   if (pipe) {
   } else if (early) {
@@ -449,8 +486,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
             // stays far inside BJ's 1e-4; keeps the 64-register budget)
             o << "        T fr" << sl_.rt << "; { R fx = " << lit(cq[0], f32) << ", fy = "
               << lit(cq[1], f32) << ";\n";
+            const auto bit = bslot.find(q);
+            if (bit != bslot.end())
+              o << "          { const T bb = bfac[itp * " << NB << " + " << bit->second
+                << "]; const R nx = fx * bb.x - fy * bb.y; fy = fx * bb.y + fy * bb.x; fx = nx; }\n";
             for (int i = eb; i < ee; i++) {
               const DiagEnt &d = ents[i];
+              if (bit != bslot.end() && d.thr_mask == 0 && d.has_base) continue;
               o << "          if (((jt & " << d.thr_mask << ") == " << d.thr_val << ")";
               if (d.has_base)
                 o << " && ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val) << ")";
@@ -613,6 +655,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   }
   if (!early) o << "    __syncthreads();\n";
   if (!pipe) o << "    b = (b + 1) % " << nbuf << ";\n";
+  if (NB) o << "    itp ^= 1;\n";
   o << "  }\n}\n";
   return o.str();
 }
