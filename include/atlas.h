@@ -186,6 +186,10 @@ const char *atlas_last_error(void);
  *                    phase's diagonal runs) [1]
  *   "shm_hoist_diag" diagonal ops move to the earliest diagonal run of their
  *                    register phase they commute back to [1]
+ *   "shm_tfac_min"   plan-specialised kernels: a diagonal slot factor whose
+ *                    conditions on the thread's tile bits number at least
+ *                    this many is evaluated once per thread into a shared
+ *                    table (0 = never) [4]
  *   "shm_pipe"       plan-specialised kernels with one tile buffer: one CTA
  *                    per SM of two thread groups sharing a ring of three
  *                    tile buffers (loads complete on mbarriers); measured

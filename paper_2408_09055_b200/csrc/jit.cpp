@@ -226,14 +226,37 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       }
     }
   const int NB = (int)bslot.size();
-  size_t off_bfac = 0;
+  // thread-only conditional factors (conditions on the thread's tile bits
+  // only): constant per thread, computed once in the prologue into a
+  // per-thread SMEM table (<= 32 KiB per CTA)
+  std::map<int, int> tslot;   // op index -> thread-factor slot
+  std::map<int, int> op_phase;
+  for (int p = 0; p < sl.nphase; p++)
+    for (int q = ph[p].op_begin; q < ph[p].op_end; q++) op_phase[q] = p;
+  if (!C->opt.shm_pipe && C->opt.shm_tfac_min > 0)
+    for (int q = 0; q < sl.nops; q++) {
+      const ShmOp &dq = ops[q];
+      if (dq.type != OP_DIAG) continue;
+      int cnt = 0;
+      for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++)
+        if (ents[i].thr_mask != 0 && !ents[i].has_base) cnt++;
+      // a table load replaces cnt compare-and-multiply steps
+      const bool any = cnt >= C->opt.shm_tfac_min;
+      if (any && (size_t)(tslot.size() + 1) * NT * esz <= 32768) {
+        const int k = (int)tslot.size();
+        tslot[q] = k;
+      }
+    }
+  int NTF = (int)tslot.size();
+  size_t off_bfac = 0, off_tfac = 0;
   auto layout = [&](int ntile_bufs, size_t &oj, size_t &os, size_t &ob, size_t &om) {
     oj = (size_t)ntile_bufs * TILE * esz;
     os = oj + (size_t)jmasks.size() * NT * 4;
     ob = (os + (size_t)smaps.size() * NT * 2 + 15) & ~(size_t)15;
     om = ob + (size_t)nbt * 256 * 8;
     off_bfac = (om + 3 * 8 + 15) & ~(size_t)15;
-    return off_bfac + (size_t)2 * NB * esz;
+    off_tfac = off_bfac + (size_t)2 * NB * esz;
+    return off_tfac + (size_t)NTF * NT * esz;
   };
   size_t off_jtab, off_stab, off_btab, off_mbar;
   // pipe: one CTA of two thread groups (each a full tile's worth of
@@ -243,6 +266,18 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   // tracked by cp.async -> mbarrier arrivals
   bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 1024 &&
               layout(3, off_jtab, off_stab, off_btab, off_mbar) + 1024 <= 233472;
+  // the thread-factor table must not cost occupancy (or exceed the opt-in
+  // limit): drop slots until it fits beside the resident CTAs
+  if (NTF) {
+    const int keep = NTF;
+    NTF = 0;
+    const size_t base_sz = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar);
+    const size_t cap = minb >= 2 ? 233472 / minb - 1024 : 232448;
+    const size_t fit = base_sz < cap ? (cap - base_sz) / ((size_t)NT * esz) : 0;
+    NTF = (int)std::min<size_t>(keep, fit);
+    for (auto it = tslot.begin(); it != tslot.end();)
+      it = it->second >= NTF ? tslot.erase(it) : std::next(it);
+  }
   const size_t smem = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar);
   const int BT = pipe ? 2 * NT : NT;  // threads per CTA
   if (pipe) minb = 1;
@@ -326,6 +361,22 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     o << " stab[" << ss * NT << " + tid] = (u16)sa; }\n";
   }
   if (pipe) o << "  }\n";
+  if (NTF) {
+    o << "  T *tfac = reinterpret_cast<T *>(smraw + " << off_tfac << ");\n";
+    for (auto &kv : tslot) {
+      const ShmOp &dq = ops[kv.first];
+      const int p = op_phase[kv.first];
+      o << "  { const int jt = (int)(jtab[" << jslot[p] * NT << " + tid] & 0xffffu); R fx = 1, fy = 0;\n";
+      for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++) {
+        const DiagEnt &d = ents[i];
+        if (!(d.thr_mask != 0 && !d.has_base)) continue;
+        o << "    if ((jt & " << d.thr_mask << ") == " << d.thr_val << ") { const R nx = fx * "
+          << lit(d.re, f32) << " - fy * " << lit(d.im, f32) << "; fy = fx * " << lit(d.im, f32)
+          << " + fy * " << lit(d.re, f32) << "; fx = nx; }\n";
+      }
+      o << "    tfac[" << kv.second * NT << " + tid].x = fx; tfac[" << kv.second * NT << " + tid].y = fy; }\n";
+    }
+  }
   // this thread's HBM offset inside a tile
   o << "  u64 off_t = 0;";
   for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) off_t |= " << u64lit(1ull << sl.act[i]) << ";";
@@ -490,9 +541,14 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
             if (bit != bslot.end())
               o << "          { const T bb = bfac[itp * " << NB << " + " << bit->second
                 << "]; const R nx = fx * bb.x - fy * bb.y; fy = fx * bb.y + fy * bb.x; fx = nx; }\n";
+            const auto tit = tslot.find(q);
+            if (tit != tslot.end())
+              o << "          { const T tt = tfac[" << tit->second * NT
+                << " + tid]; const R nx = fx * tt.x - fy * tt.y; fy = fx * tt.y + fy * tt.x; fx = nx; }\n";
             for (int i = eb; i < ee; i++) {
               const DiagEnt &d = ents[i];
               if (bit != bslot.end() && d.thr_mask == 0 && d.has_base) continue;
+              if (tit != tslot.end() && d.thr_mask != 0 && !d.has_base) continue;
               o << "          if (((jt & " << d.thr_mask << ") == " << d.thr_val << ")";
               if (d.has_base)
                 o << " && ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val) << ")";
