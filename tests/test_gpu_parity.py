@@ -257,3 +257,22 @@ def test_ghz_n33():
         got = _amps(s, idx)
     want = np.array([2 ** -0.5 if i in (0, (1 << n) - 1) else 0.0 for i in idx])
     assert np.abs(got - want).max() <= 1e-10
+
+
+def test_qft_n34_fp32_basis_state():
+    """fp32 at the single-GPU capacity: 2^34 complex64 amplitudes = 128 GiB
+    (BASELINE config 5's fp32 shard size is 2^33 per GPU on 8 GPUs),
+    qft from |x> against the P4 closed form within BJ's fp32 tolerance."""
+    n = 34
+    x = 0x2B5A3C1F7 & ((1 << n) - 1)
+    c = C.prepend_basis(C.qft(n), x)
+    rev = int(format(x, f"0{n}b")[::-1], 2)
+    with A.Simulator(n, 1, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.run()
+        idx = _sample_idx(n, 64, 7)
+        got = _amps(s, idx).astype(np.complex128)
+    want = np.array([np.exp(2j * np.pi * ((rev * y) % (1 << n)) / (1 << n)) for y in idx]) * 2 ** (-n / 2)
+    # fp32: relative to the amplitude scale 2^{-17}
+    assert np.abs(got - want).max() <= 1e-4 * 2 ** (-n / 2) * 64
