@@ -186,6 +186,10 @@ const char *atlas_last_error(void);
  *                    phase's diagonal runs) [1]
  *   "shm_hoist_diag" diagonal ops move to the earliest diagonal run of their
  *                    register phase they commute back to [1]
+ *   "shm_swz_phase"  plan-specialised kernels: a permuted phase store may pick
+ *                    its own XOR swizzle of the tile layout (and the lanes
+ *                    of each phase are re-chosen) so that stores and gathers
+ *                    are bank-conflict free [1]
  *   "shm_tfac_min"   plan-specialised kernels: a diagonal slot factor whose
  *                    conditions on the thread's tile bits number at least
  *                    this many is evaluated once per thread into a shared

@@ -23,7 +23,9 @@
 #include <atomic>
 #include <complex>
 #include <map>
+#include <random>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -174,28 +176,194 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   const PermTerm *terms = C->terms.data() + sl.term_off;
   int minb = (nbuf == 1 && (K - RB) >= 8 && (K - RB) <= 9 && (esz << K) <= 65536) ? 2 : 1;
 
-  // distinct thread-index tables: jt per register mask, store offsets per
-  // (register mask, permuted images)
-  std::vector<int> rmask(sl.nphase), jslot(sl.nphase), sslot(sl.nphase, -1);
-  std::vector<int> jmasks;  // register mask | qlane << 16
-  std::vector<std::pair<int, std::vector<uint16_t>>> smaps;
+  // ---- shared-memory swizzles per phase boundary and lanes per phase.
+  // A swizzle is S(j) = j ^ sum_{b >= W} j_b * col[b] (col[b] < 2^W): linear,
+  // an involution, and the identity on the W lowest tile bits (the lanes of
+  // the cp.async load and of the copy-out).  Phase p gathers from the layout
+  // of boundary p-1 and stores into that of boundary p; the layout of the
+  // first load is the global swizzle (device.h).  A permuted phase may pick a
+  // new layout for its store so that both its store and the next phase's
+  // gather hit W independent bank groups (for the 8 / 16 lanes of one
+  // wavefront) where the global swizzle cannot.
+  const int W = f32 ? 4 : 3;
+  const unsigned WM = (1u << W) - 1;
+  typedef std::vector<unsigned> Swz;
+  std::vector<Swz> swzs(1, Swz(K, 0));
+  for (int b = W; b < K; b++) swzs[0][b] = 1u << (b % W);
+  auto Sx = [&](const Swz &c, unsigned j) {
+    unsigned r = j;
+    for (int b = W; b < K; b++)
+      if ((j >> b) & 1) r ^= c[b];
+    return r;
+  };
+  auto rank_w = [&](const std::vector<unsigned> &vs) {
+    unsigned basis[16] = {0};
+    int r = 0;
+    for (unsigned v : vs) {
+      v &= WM;
+      for (int bit = W - 1; bit >= 0 && v; bit--)
+        if ((v >> bit) & 1) {
+          if (!basis[bit]) {
+            basis[bit] = v;
+            r++;
+            v = 0;
+          } else {
+            v ^= basis[bit];
+          }
+        }
+    }
+    return r;
+  };
+  // unswizzled folded map of each permuted phase (the lowering stores it
+  // under the global swizzle, an involution)
+  std::vector<std::vector<unsigned>> Acol(sl.nphase);
+  std::vector<unsigned> Ac0(sl.nphase, 0);
+  for (int p = 0; p < sl.nphase; p++)
+    if (ph[p].permuted) {
+      Acol[p].resize(K);
+      for (int b = 0; b < K; b++) Acol[p][b] = Sx(swzs[0], ph[p].colimg[b]);
+      Ac0[p] = Sx(swzs[0], ph[p].c0_swz);
+    }
+  const int lastp = sl.nphase - 1;
+  const bool ld_ = sl.last_direct != 0;
+  std::vector<int> rmask(sl.nphase), gsw(sl.nphase, 0), ssw(sl.nphase, 0);
+  std::vector<unsigned> qln(sl.nphase, 0xffff);
   for (int p = 0; p < sl.nphase; p++) {
     int m = 0;
     for (int i = 0; i < RB; i++) m |= 1 << ph[p].rbit[i];
     rmask[p] = m;
-    const int key = m | ((int)ph[p].qlane << 16);
+  }
+  auto subsets = [&](int p) {
+    // candidate lane sets: the lowering's choice, the default, then all
+    std::vector<std::vector<int>> out;
+    std::vector<int> nr;
+    for (int b = 0; b < K; b++)
+      if (!((rmask[p] >> b) & 1)) nr.push_back(b);
+    if ((int)nr.size() < W) return out;
+    if (ph[p].qlane != 0xffff) {
+      std::vector<int> q;
+      for (int i = 0; i < W; i++) q.push_back((ph[p].qlane >> (4 * i)) & 15);
+      out.push_back(q);
+    }
+    out.push_back(std::vector<int>(nr.begin(), nr.begin() + W));
+    const int nn = (int)nr.size();
+    for (unsigned mm = 0; mm < (1u << nn); mm++) {
+      if (__builtin_popcount(mm) != W) continue;
+      std::vector<int> q;
+      for (int i = 0; i < nn; i++)
+        if ((mm >> i) & 1) q.push_back(nr[i]);
+      out.push_back(q);
+    }
+    return out;
+  };
+  auto gather_rank = [&](const std::vector<int> &sub, const Swz &G) {
+    std::vector<unsigned> v;
+    for (int b : sub) v.push_back(Sx(G, 1u << b));
+    return rank_w(v);
+  };
+  auto store_rank = [&](int p, const std::vector<int> &sub, const Swz &T) {
+    std::vector<unsigned> v;
+    for (int b : sub) v.push_back(Sx(T, Acol[p][b]));
+    return rank_w(v);
+  };
+  auto enc = [&](const std::vector<int> &sub) {
+    unsigned q = 0xffff;
+    for (int i = 0; i < (int)sub.size(); i++) q = (q & ~(15u << (4 * i))) | ((unsigned)sub[i] << (4 * i));
+    return q;
+  };
+  std::mt19937 rng(12345u);  // deterministic: identical on every rank
+  for (int p = 0; p < sl.nphase; p++) {
+    const Swz G = swzs[gsw[p]];
+    const auto subs = subsets(p);
+    if (subs.empty()) continue;
+    if (ld_ && p == lastp) {  // direct store: lanes = tile bits 0..4
+      ssw[p] = gsw[p];
+      continue;
+    }
+    const bool perm = ph[p].permuted != 0;
+    const bool swz_free = C->opt.shm_swz_phase != 0;
+    // best gather-only choice (fallback)
+    std::vector<int> best = subs[0];
+    int bestr = -1;
+    for (auto &sub : subs) {
+      const int r = gather_rank(sub, G) + (perm ? store_rank(p, sub, G) : W);
+      if (r > bestr) {
+        bestr = r;
+        best = sub;
+      }
+    }
+    qln[p] = enc(best);
+    ssw[p] = gsw[p];
+    if (p + 1 < sl.nphase) gsw[p + 1] = gsw[p];
+    if (!perm || !swz_free || bestr == 2 * W) continue;
+    // a permuted phase whose store conflicts: look for a store layout
+    bool done = false;
+    for (int trial = 0; trial < 400 && !done; trial++) {
+      Swz T(K, 0);
+      if (trial == 0) T = swzs[0];
+      else
+        for (int b = W; b < K; b++) T[b] = rng() & WM;
+      for (auto &sub : subs) {
+        if (gather_rank(sub, G) != W || store_rank(p, sub, T) != W) continue;
+        // the next phase must find a conflict-free gather under T
+        bool next_ok = p + 1 >= sl.nphase;
+        if (!next_ok)
+          for (auto &s2 : subsets(p + 1))
+            if (gather_rank(s2, T) == W) {
+              next_ok = true;
+              break;
+            }
+        if (!next_ok) continue;
+        int ti = -1;
+        for (size_t i = 0; i < swzs.size(); i++)
+          if (swzs[i] == T) ti = (int)i;
+        if (ti < 0) {
+          ti = (int)swzs.size();
+          swzs.push_back(T);
+        }
+        qln[p] = enc(sub);
+        ssw[p] = ti;
+        if (p + 1 < sl.nphase) gsw[p + 1] = ti;
+        done = true;
+        break;
+      }
+    }
+  }
+  if (getenv("ATLAS_DEBUG_SWZ"))
+    for (int p = 0; p < sl.nphase; p++) {
+      std::vector<int> sub;
+      if (qln[p] != 0xffff)
+        for (int i = 0; i < W; i++) sub.push_back((qln[p] >> (4 * i)) & 15);
+      else
+        for (int b = 0; b < K && (int)sub.size() < W; b++)
+          if (!((rmask[p] >> b) & 1)) sub.push_back(b);
+      fprintf(stderr, "swz phase %d perm %d gather %d store %d layouts %d/%d\n", p, (int)ph[p].permuted,
+              gather_rank(sub, swzs[gsw[p]]),
+              ph[p].permuted && !(ld_ && p == lastp) ? store_rank(p, sub, swzs[ssw[p]]) : W, gsw[p], ssw[p]);
+    }
+  // distinct thread-index tables: (register mask, lanes, gather layout) ->
+  // jt and its gather address; (register mask, lanes, store images) -> the
+  // permuted store address
+  std::vector<int> jslot(sl.nphase), sslot(sl.nphase, -1);
+  std::vector<std::pair<long long, int>> jmasks;  // (mask | lanes << 16, layout)
+  std::vector<std::pair<int, std::vector<uint16_t>>> smaps;
+  std::vector<std::vector<uint16_t>> simg(sl.nphase);
+  for (int p = 0; p < sl.nphase; p++) {
+    const int key = rmask[p] | ((int)qln[p] << 16);
     int js = -1;
     for (size_t i = 0; i < jmasks.size(); i++)
-      if (jmasks[i] == key) js = (int)i;
+      if (jmasks[i].first == key && jmasks[i].second == gsw[p]) js = (int)i;
     if (js < 0) {
       js = (int)jmasks.size();
-      jmasks.push_back(key);
+      jmasks.push_back({key, gsw[p]});
     }
     jslot[p] = js;
     if (ph[p].permuted) {
-      std::vector<uint16_t> img(ph[p].colimg, ph[p].colimg + K);
+      std::vector<uint16_t> img(K);
+      for (int b = 0; b < K; b++) img[b] = (uint16_t)Sx(swzs[ssw[p]], Acol[p][b]);
+      simg[p] = img;
       int ss = -1;
-        for (size_t i = 0; i < smaps.size(); i++)
+      for (size_t i = 0; i < smaps.size(); i++)
         if (smaps[i].first == key && smaps[i].second == img) ss = (int)i;
       if (ss < 0) {
         ss = (int)smaps.size();
@@ -348,10 +516,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   };
   if (pipe) o << "  if (grp == 0) {\n";
   for (size_t js = 0; js < jmasks.size(); js++) {
-    o << "  { int jt = 0;";
-    const std::vector<int> ord = thread_order(jmasks[js]);
-    for (size_t t = 0; t < ord.size(); t++) o << " jt |= ((tid >> " << t << ") & 1) << " << ord[t] << ";";
-    o << " jtab[" << js * NT << " + tid] = ((u32)swz(jt) << 16) | (u32)jt; }\n";
+    o << "  { int jt = 0; u32 sj = 0;";
+    const std::vector<int> ord = thread_order((int)jmasks[js].first);
+    const Swz &G = swzs[jmasks[js].second];
+    for (size_t t = 0; t < ord.size(); t++)
+      o << " if ((tid >> " << t << ") & 1) { jt |= " << (1 << ord[t]) << "; sj ^= " << Sx(G, 1u << ord[t])
+        << "u; }";
+    o << " jtab[" << js * NT << " + tid] = (sj << 16) | (u32)jt; }\n";
   }
   for (size_t ss = 0; ss < smaps.size(); ss++) {
     o << "  { u32 sa = 0;";
@@ -381,6 +552,11 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   o << "  u64 off_t = 0;";
   for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) off_t |= " << u64lit(1ull << sl.act[i]) << ";";
   o << "\n  const int sw_tid = swz(tid);\n";
+  // copy-out reads the layout of the last boundary
+  const Swz &SO = swzs[ssw[lastp]];
+  o << "  int sw_out = 0;";
+  for (int t = 0; t < K - RB; t++) o << " if ((tid >> " << t << ") & 1) sw_out ^= " << Sx(SO, 1u << t) << ";";
+  o << "\n";
   o << "  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);\n";
   o << "  __syncthreads();\n";
   o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255]";
@@ -490,7 +666,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   for (int p = 0; p < sl.nphase; p++) {
     const ShmPhase &P = ph[p];
     int sr[4] = {0, 0, 0, 0};
-    for (int i = 0; i < RB; i++) sr[i] = swz(1 << P.rbit[i]);
+    for (int i = 0; i < RB; i++) sr[i] = (int)Sx(swzs[gsw[p]], 1u << P.rbit[i]);
     o << "    { // phase " << p << "\n";
     o << "      const u32 jj = jtab[" << jslot[p] * NT << " + tid]; const int jt = (int)(jj & 0xffffu); "
       << "const int sj = (int)(jj >> 16); (void)jt;\n";
@@ -675,16 +851,16 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       break;
     }
     if (P.permuted) {
-      o << "      u32 cb = " << P.c0_swz << "u;\n";
+      o << "      u32 cb = " << Sx(swzs[ssw[p]], Ac0[p]) << "u;\n";
       for (int i = P.term_begin; i < P.term_end; i++)
         o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
-          << ") cb ^= " << terms[i].vec_swz << "u;\n";
+          << ") cb ^= " << Sx(swzs[ssw[p]], Sx(swzs[0], terms[i].vec_swz)) << "u;\n";
       o << "      const int s0 = (int)(stab[" << sslot[p] * NT << " + tid] ^ cb);\n";
       o << "      " << GS << "\n";
       for (int e = 0; e < NE; e++) {
         int a = 0;
         for (int i = 0; i < RB; i++)
-          if ((e >> i) & 1) a ^= P.colimg[P.rbit[i]];
+          if ((e >> i) & 1) a ^= simg[p][P.rbit[i]];
         o << "      tb[s0 ^ " << a << "] = v[" << e << "];\n";
       }
     } else {
@@ -700,12 +876,12 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   if (!ld) {
     o << "    { T *g = st + base + off_t;\n";
     if (early) {
-      for (int it = 0; it < NE; it++) o << "      v[" << it << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
+      for (int it = 0; it < NE; it++) o << "      v[" << it << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
       o << "      " << GS << "\n      " << next_issue << "\n";
       for (int it = 0; it < NE; it++) o << "      g[" << u64lit(itoff[it]) << "] = v[" << it << "];\n";
     } else {
       for (int it = 0; it < NE; it++)
-        o << "      g[" << u64lit(itoff[it]) << "] = tb[sw_tid ^ " << swz(it * NT) << "];\n";
+        o << "      g[" << u64lit(itoff[it]) << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
     }
     o << "    }\n";
   }
