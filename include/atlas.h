@@ -186,6 +186,10 @@ const char *atlas_last_error(void);
  *                    phase's diagonal runs) [1]
  *   "shm_hoist_diag" diagonal ops move to the earliest diagonal run of their
  *                    register phase they commute back to [1]
+ *   "shm_defer_scalar" plan-specialised kernels: unconditional real blocks
+ *                    with entries of equal magnitude (H) run as adds; the
+ *                    uniform scale is folded into a later block or applied
+ *                    once before the kernel's last store [1]
  *   "shm_swz_phase"  plan-specialised kernels: a permuted phase store may pick
  *                    its own XOR swizzle of the tile layout (and the lanes
  *                    of each phase are re-chosen) so that stores and gathers

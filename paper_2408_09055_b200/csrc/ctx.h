@@ -71,6 +71,7 @@ struct Options {
   int front = 1;
   int shm_split_dense = 1;   // complex 2x2 blocks -> D1 R D2 (real R) in SHM kernels
   int shm_hoist_diag = 1;    // diagonal ops join the earliest reachable diagonal run
+  int shm_defer_scalar = 1;  // JIT: H-type blocks as adds, their uniform scale deferred
   int shm_swz_phase = 1;     // JIT: per-boundary SMEM swizzles for permuted stores
   int shm_tfac_min = 4;      // JIT: thread-only factor tables for slots with >= this many entries (0: off)
   int shm_pipe = 0;          // JIT: two thread groups per CTA on a ring of 3 tile buffers

@@ -21,6 +21,7 @@
 #include <dlfcn.h>
 
 #include <atomic>
+#include <cmath>
 #include <complex>
 #include <map>
 #include <random>
@@ -663,6 +664,8 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   if (!pipe) o << "    __syncthreads();\n";
   o << "    T *tb = buf + b * " << TILE << ";\n";
   o << "    T v[" << NE << "];\n";
+  double pend = 1.0;  // deferred uniform scalar (sign blocks)
+  const bool defer_scalar = C->opt.shm_defer_scalar != 0;
   for (int p = 0; p < sl.nphase; p++) {
     const ShmPhase &P = ph[p];
     int sr[4] = {0, 0, 0, 0};
@@ -801,11 +804,41 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
           break;
         case OP_DENSE1: {
           const int tb = op.t0;
+          // an unconditional real block c * (+-1 entries) (H and its sign
+          // variants): adds/subtracts only; the uniform factor c is deferred
+          // (a scalar on every amplitude commutes with every op) and folded
+          // into the next unconditional general block, else applied once
+          // before the kernel's last store
+          const bool sign_blk = full && defer_scalar && c[1] == 0 && c[3] == 0 && c[5] == 0 && c[7] == 0 &&
+                                c[0] != 0 && std::abs(c[2]) == std::abs(c[0]) &&
+                                std::abs(c[4]) == std::abs(c[0]) && std::abs(c[6]) == std::abs(c[0]);
+          if (sign_blk) {
+            const double k = std::abs(c[0]);
+            pend *= k;
+            const char *sg[4];
+            for (int i = 0; i < 4; i++) sg[i] = c[2 * i] > 0 ? "+" : "-";
+            for (int e = 0; e < NE; e++) {
+              if (e & (1 << tb)) continue;
+              const int e1 = e | (1 << tb);
+              o << ind << "{ const T x0 = v[" << e << "], x1 = v[" << e1 << "];";
+              for (int r = 0; r < 2; r++)
+                for (int part = 0; part < 2; part++) {
+                  const char *f = part ? "y" : "x";
+                  o << " v[" << (r ? e1 : e) << "]." << f << " = " << sg[2 * r] << "x0." << f << " "
+                    << sg[2 * r + 1] << " x1." << f << ";";
+                }
+              o << " }\n";
+            }
+            break;
+          }
+          double cs[8];
+          for (int i = 0; i < 8; i++) cs[i] = c[i] * (full ? pend : 1.0);
+          if (full) pend = 1.0;
           for (int e = 0; e < NE; e++) {
             if (e & (1 << tb)) continue;
             if (!((em >> e) & 1)) continue;
             const int idx[2] = {e, e | (1 << tb)};
-            emit_block(o, 2, idx, c, f32, ind);
+            emit_block(o, 2, idx, cs, f32, ind);
           }
           break;
         }
@@ -830,6 +863,11 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
         }
       }
       if (!full) o << "      }\n";
+    }
+    if (p == last && pend != 1.0) {
+      for (int e = 0; e < NE; e++)
+        o << "      v[" << e << "].x *= " << lit(pend, f32) << "; v[" << e << "].y *= " << lit(pend, f32) << ";\n";
+      pend = 1.0;
     }
     if (ld && p == last) {
       uint64_t limg[4] = {0, 0, 0, 0};
