@@ -831,6 +831,72 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
             }
             break;
           }
+          // an unconditional real rotation [[a,-b],[b,a]] or reflection
+          // [[a,b],[b,-a]]: factor out the larger of |a|, |b| (deferred like
+          // the sign blocks), leaving one FMA per output component
+          if (full && defer_scalar && c[1] == 0 && c[3] == 0 && c[5] == 0 && c[7] == 0) {
+            const double a = c[0], b = c[4], m01 = c[2], m11 = c[6];
+            const double tol = 1e-15 * (std::abs(a) + std::abs(b));
+            const bool rot = std::abs(m11 - a) <= tol && std::abs(m01 + b) <= tol;
+            const bool refl = std::abs(m11 + a) <= tol && std::abs(m01 - b) <= tol;
+            if ((rot || refl) && a != 0 && b != 0) {
+              const bool big_a = std::abs(a) >= std::abs(b);
+              const double k = big_a ? a : b, t = big_a ? b / a : a / b;
+              pend *= k;
+              const std::string T_ = lit(t, f32), NT_ = lit(-t, f32);
+              for (int e = 0; e < NE; e++) {
+                if (e & (1 << tb)) continue;
+                const int e1 = e | (1 << tb);
+                o << ind << "{ const T x0 = v[" << e << "], x1 = v[" << e1 << "];";
+                for (int part = 0; part < 2; part++) {
+                  const char *f = part ? "y" : "x";
+                  std::string y0, y1;
+                  const std::string X0 = std::string("x0.") + f, X1 = std::string("x1.") + f;
+                  if (rot && big_a) {        // (x0 - t x1, t x0 + x1)
+                    y0 = "fma(" + NT_ + ", " + X1 + ", " + X0 + ")";
+                    y1 = "fma(" + T_ + ", " + X0 + ", " + X1 + ")";
+                  } else if (rot) {          // (t x0 - x1, x0 + t x1)
+                    y0 = "fma(" + T_ + ", " + X0 + ", -" + X1 + ")";
+                    y1 = "fma(" + T_ + ", " + X1 + ", " + X0 + ")";
+                  } else if (big_a) {        // (x0 + t x1, t x0 - x1)
+                    y0 = "fma(" + T_ + ", " + X1 + ", " + X0 + ")";
+                    y1 = "fma(" + T_ + ", " + X0 + ", -" + X1 + ")";
+                  } else {                   // (t x0 + x1, x0 - t x1)
+                    y0 = "fma(" + T_ + ", " + X0 + ", " + X1 + ")";
+                    y1 = "fma(" + NT_ + ", " + X1 + ", " + X0 + ")";
+                  }
+                  o << " v[" << e << "]." << f << " = " << y0 << "; v[" << e1 << "]." << f << " = " << y1 << ";";
+                }
+                o << " }\n";
+              }
+              break;
+            }
+          }
+          // an unconditional [[a, ib], [ib, a]] (RX type): factor out the
+          // larger of |a|, |b| likewise
+          if (full && defer_scalar && c[1] == 0 && c[7] == 0 && c[2] == 0 && c[4] == 0 && c[0] == c[6] &&
+              c[3] == c[5] && c[0] != 0 && c[3] != 0) {
+            const double a = c[0], b = c[3];
+            const bool big_a = std::abs(a) >= std::abs(b);
+            const double k = big_a ? a : b, t = big_a ? b / a : a / b;
+            pend *= k;
+            const std::string T_ = lit(t, f32), NT_ = lit(-t, f32);
+            for (int e = 0; e < NE; e++) {
+              if (e & (1 << tb)) continue;
+              const int e1 = e | (1 << tb);
+              o << ind << "{ const T x0 = v[" << e << "], x1 = v[" << e1 << "];";
+              if (big_a)  // y0 = x0 + i t x1, y1 = i t x0 + x1
+                o << " v[" << e << "].x = fma(" << NT_ << ", x1.y, x0.x); v[" << e << "].y = fma(" << T_
+                  << ", x1.x, x0.y); v[" << e1 << "].x = fma(" << NT_ << ", x0.y, x1.x); v[" << e1
+                  << "].y = fma(" << T_ << ", x0.x, x1.y);";
+              else  // y0 = t x0 + i x1, y1 = i x0 + t x1
+                o << " v[" << e << "].x = fma(" << T_ << ", x0.x, -x1.y); v[" << e << "].y = fma(" << T_
+                  << ", x0.y, x1.x); v[" << e1 << "].x = fma(" << T_ << ", x1.x, -x0.y); v[" << e1
+                  << "].y = fma(" << T_ << ", x1.y, x0.x);";
+              o << " }\n";
+            }
+            break;
+          }
           double cs[8];
           for (int i = 0; i < 8; i++) cs[i] = c[i] * (full ? pend : 1.0);
           if (full) pend = 1.0;
