@@ -168,7 +168,8 @@ const char *atlas_last_error(void);
  *                    cost model's value (5), see "ls_auto"]
  *   "ls_auto"        with ls_qubits unset and the built-in cost model, also
  *                    plan with one forced qubit fewer and keep the plan of
- *                    lower model cost (ties: the model's value) [1]
+ *                    lower model cost (ties: the model's value), as long as
+ *                    contiguous runs stay >= 256 B (fp64 4, fp32 5) [1]
  *   "shm_qubits"     override q_max_shared of the cost model [model]
  *   "fusion_qubits"  override q_max_fusion of the cost model [model]
  *   "kinds"          bit 0 fusion, bit 1 shared-memory [3]

@@ -113,8 +113,11 @@ atlas_status atlas_plan(atlas_ctx *C, int s_max, double c) {
     // least-significant qubit fewer (256-B runs stream as well as 512-B runs
     // on B200 HBM3e, and a tile then spans one more high qubit) and keep the
     // plan of lower model cost (ties: the model's setting)
+    // contiguous runs stay >= 256 B (fp64: ls >= 4, fp32: ls >= 5); 128-B
+    // runs measured slower per pass (fp32 su2random n=28: 11.4 vs 11.0 ms)
+    const int ls_min = C->dt == ATLAS_C128 ? 4 : 5;
     if (C->opt.ls_qubits < 0 && C->opt.cost_model.empty() && C->opt.ls_auto &&
-        C->cm.ls_qubits > 3) {
+        C->cm.ls_qubits - 1 >= ls_min) {
       auto total = [&]() {
         int64_t t = 0;
         for (auto &kp : C->kplans) t += kp.total;
