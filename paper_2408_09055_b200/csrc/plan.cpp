@@ -1138,7 +1138,6 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                     bsel = sel;
                   }
                 }
-                if (getenv("ATLAS_DEBUG_QLANE")) fprintf(stderr, "qlane: permuted=%d default=%d best=%d R=%x\n", (int)ph.permuted, cost(def), best, rm);
                 if (!bsel.empty()) {
                   u32 q = 0xffff;
                   for (int i = 0; i < W; i++) q = (q & ~(15u << (4 * i))) | ((u32)bsel[i] << (4 * i));
