@@ -201,8 +201,7 @@ const char *atlas_last_error(void);
  *                    table (0 = never) [4]
  *   "shm_pipe"       plan-specialised kernels with one tile buffer: one CTA
  *                    per SM of two thread groups sharing a ring of three
- *                    tile buffers (loads complete on mbarriers); measured
- *                    slower than 2 CTAs of one buffer on n=28 [0]
+ *                    tile buffers (loads complete on mbarriers) [1]
  *   "shm_ctas"       plan-specialised kernels of 2^12-amplitude fp64 tiles:
  *                    resident CTAs per SM, 2 (128 registers) or 3 (80
  *                    registers, when their shared memory fits) [2]

@@ -74,7 +74,7 @@ struct Options {
   int shm_defer_scalar = 1;  // JIT: H-type blocks as adds, their uniform scale deferred
   int shm_swz_phase = 1;     // JIT: per-boundary SMEM swizzles for permuted stores
   int shm_tfac_min = 4;      // JIT: thread-only factor tables for slots with >= this many entries (0: off)
-  int shm_pipe = 0;          // JIT: two thread groups per CTA on a ring of 3 tile buffers
+  int shm_pipe = 1;          // JIT: two thread groups per CTA on a ring of 3 tile buffers
   int shm_ctas = 2;          // JIT: resident SHM CTAs per SM for 2^12 fp64 tiles (2 or 3)
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter
   long long dp_budget = 1000000;

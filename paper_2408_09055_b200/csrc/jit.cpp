@@ -382,18 +382,17 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   // by one designated thread per slot into a double-buffered SMEM table
   // instead of by every thread
   std::map<int, int> bslot;  // op index -> base-factor slot
-  if (!C->opt.shm_pipe)
-    for (int q = 0; q < sl.nops; q++) {
-      const ShmOp &dq = ops[q];
-      if (dq.type != OP_DIAG) continue;
-      bool any = false;
-      for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++)
-        if (ents[i].thr_mask == 0 && ents[i].has_base) any = true;
-      if (any) {
-        const int k = (int)bslot.size();
-        bslot[q] = k;
-      }
+  for (int q = 0; q < sl.nops; q++) {
+    const ShmOp &dq = ops[q];
+    if (dq.type != OP_DIAG) continue;
+    bool any = false;
+    for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++)
+      if (ents[i].thr_mask == 0 && ents[i].has_base) any = true;
+    if (any) {
+      const int k = (int)bslot.size();
+      bslot[q] = k;
     }
+  }
   const int NB = (int)bslot.size();
   // thread-only conditional factors (conditions on the thread's tile bits
   // only): constant per thread, computed once in the prologue into a
@@ -402,7 +401,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   std::map<int, int> op_phase;
   for (int p = 0; p < sl.nphase; p++)
     for (int q = ph[p].op_begin; q < ph[p].op_end; q++) op_phase[q] = p;
-  if (!C->opt.shm_pipe && C->opt.shm_tfac_min > 0)
+  if (C->opt.shm_tfac_min > 0)
     for (int q = 0; q < sl.nops; q++) {
       const ShmOp &dq = ops[q];
       if (dq.type != OP_DIAG) continue;
@@ -424,8 +423,8 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     ob = (os + (size_t)smaps.size() * NT * 2 + 15) & ~(size_t)15;
     om = ob + (size_t)nbt * 256 * 8;
     off_bfac = (om + 3 * 8 + 15) & ~(size_t)15;
-    off_tfac = off_bfac + (size_t)2 * NB * esz;
-    return off_tfac + (size_t)NTF * NT * esz;
+    off_tfac = off_bfac + (size_t)4 * NB * esz;
+    return off_tfac + (size_t)NTF * NT * esz;  // bfac: [group][parity][slot]
   };
   size_t off_jtab, off_stab, off_btab, off_mbar;
   // pipe: one CTA of two thread groups (each a full tile's worth of
@@ -535,6 +534,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   if (pipe) o << "  }\n";
   if (NTF) {
     o << "  T *tfac = reinterpret_cast<T *>(smraw + " << off_tfac << ");\n";
+    if (pipe) o << "  if (grp == 0) {\n";
     for (auto &kv : tslot) {
       const ShmOp &dq = ops[kv.first];
       const int p = op_phase[kv.first];
@@ -548,6 +548,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       }
       o << "    tfac[" << kv.second * NT << " + tid].x = fx; tfac[" << kv.second * NT << " + tid].y = fy; }\n";
     }
+    if (pipe) o << "  }\n";
   }
   // this thread's HBM offset inside a tile
   o << "  u64 off_t = 0;";
@@ -652,6 +653,27 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       << "].y = fy; }\n";
   }
   }
+  if (pipe && NB) {
+    // per group: its own double-buffered table, a designated thread of the
+    // group, and a group barrier before the factors are read
+    const int gw = NT / 32;
+    for (auto &kv : bslot) {
+      const int bk = kv.second;
+      const ShmOp &dq = ops[kv.first];
+      const int desig = (bk % gw) * 32 + (bk / gw) % 32;
+      o << "    if (tid == " << desig << ") { R fx = 1, fy = 0;\n";
+      for (int i = (int)dq.base_mask; i < (int)dq.base_val; i++) {
+        const DiagEnt &d = ents[i];
+        if (!(d.thr_mask == 0 && d.has_base)) continue;
+        o << "      if ((base & " << u64lit(d.base_mask) << ") == " << u64lit(d.base_val)
+          << ") { const R nx = fx * " << lit(d.re, f32) << " - fy * " << lit(d.im, f32) << "; fy = fx * "
+          << lit(d.im, f32) << " + fy * " << lit(d.re, f32) << "; fx = nx; }\n";
+      }
+      o << "      bfac[(grp * 2 + itp) * " << NB << " + " << bk << "].x = fx; bfac[(grp * 2 + itp) * " << NB
+        << " + " << bk << "].y = fy; }\n";
+    }
+    o << "    gsync(grp);\n";
+  }
   if (pipe) {
   } else if (early) {
     o << "    asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
@@ -718,8 +740,8 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
               << lit(cq[1], f32) << ";\n";
             const auto bit = bslot.find(q);
             if (bit != bslot.end())
-              o << "          { const T bb = bfac[itp * " << NB << " + " << bit->second
-                << "]; const R nx = fx * bb.x - fy * bb.y; fy = fx * bb.y + fy * bb.x; fx = nx; }\n";
+              o << "          { const T bb = bfac[" << (pipe ? "(grp * 2 + itp) * " : "itp * ") << NB << " + "
+                << bit->second << "]; const R nx = fx * bb.x - fy * bb.y; fy = fx * bb.y + fy * bb.x; fx = nx; }\n";
             const auto tit = tslot.find(q);
             if (tit != tslot.end())
               o << "          { const T tt = tfac[" << tit->second * NT

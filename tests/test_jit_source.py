@@ -56,9 +56,10 @@ def test_jit_sources_compile_without_spills(fam, dtype, tmp_path):
         threads, minb = int(m.group(1)), int(m.group(2))
         regs, spill = ptxas(src, tmp_path, f"k{i}")
         assert regs * threads * minb <= 65536
-        # fp32 2^13 tiles run 512 threads x 2 CTAs at <= 64 registers: a few
-        # bytes of spill around conditional diagonal factors are tolerated
-        assert spill <= (0 if dtype == 0 else 32), f"kernel {i} spills {spill} bytes"
+        # at the register cap (128 for the 512-thread two-group CTA, 64 for
+        # fp32's 2 x 512 threads) a few bytes of spill around conditional
+        # diagonal factors are tolerated; more is a code-generation regression
+        assert spill <= (16 if dtype == 0 else 32), f"kernel {i} spills {spill} bytes"
 
 
 def test_jit_source_reflects_program():
