@@ -432,7 +432,9 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   // load is issued into the buffer the other group just finished with, so up
   // to two loads are in flight while both groups compute; completion is
   // tracked by cp.async -> mbarrier arrivals
-  bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 1024 &&
+  // (two groups of 256: the fp64 2^12 tiles; fp32's 2 x 512 threads at 64
+  // registers measured slower than two single-buffer CTAs)
+  bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 512 &&
               layout(3, off_jtab, off_stab, off_btab, off_mbar) + 1024 <= 233472;
   // the thread-factor table must not cost occupancy (or exceed the opt-in
   // limit): drop slots until it fits beside the resident CTAs
