@@ -19,42 +19,58 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sv_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+_LIB = os.path.join(_HERE, "liboracle.so")          # 1 thread
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")  # OpenMP over the host cores
 
 # The oracle's own kind codes (order of the enum in sv_oracle.c).
 KIND_CODE = {k: i for i, k in enumerate(
     ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "P", "U3",
      "CX", "CZ", "CP", "CCX", "SWAP", "CU"])}
 
-_lib = None
+_libs = {}
+
+
+def _build_one(out, extra, force):
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", *extra,
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
 
 
 def build(force: bool = False) -> str:
-    """Compile sv_oracle.c with plain gcc (-O2, no fast-math)."""
-    if force or not os.path.exists(_LIB) or \
-            os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """Compile sv_oracle.c with plain gcc (-O2, no fast-math) twice: a
+    single-threaded build and an OpenMP build of the same loops (the gate
+    loop over amplitude groups split across host cores; identical
+    arithmetic per amplitude, so both give bit-identical states)."""
+    _build_one(_LIB_OMP, ["-fopenmp"], force)
+    return _build_one(_LIB, [], force)
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(omp: bool = True):
+    """The oracle library: the OpenMP build (default) or the 1-thread one."""
+    key = bool(omp)
+    if key not in _libs:
         build()
-        _lib = ctypes.CDLL(_LIB)
-        _lib.oracle_simulate.restype = ctypes.c_int
-        _lib.oracle_simulate.argtypes = [
+        L = ctypes.CDLL(_LIB_OMP if omp else _LIB)
+        L.oracle_simulate.restype = ctypes.c_int
+        L.oracle_simulate.argtypes = [
             ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
-        _lib.oracle_gate_matrix.restype = ctypes.c_int
-        _lib.oracle_gate_matrix.argtypes = [ctypes.c_int, ctypes.c_void_p,
-                                            ctypes.c_void_p, ctypes.c_void_p]
-        _lib.oracle_norm2.restype = ctypes.c_double
-        _lib.oracle_norm2.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    return _lib
+        L.oracle_gate_matrix.restype = ctypes.c_int
+        L.oracle_gate_matrix.argtypes = [ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_norm2.restype = ctypes.c_double
+        L.oracle_norm2.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.oracle_threads.restype = ctypes.c_int
+        _libs[key] = L
+    return _libs[key]
+
+
+def threads(omp: bool = True) -> int:
+    """Host threads the chosen build runs on."""
+    return lib(omp).oracle_threads()
 
 
 def encode(gates):
@@ -69,9 +85,10 @@ def encode(gates):
     return kinds, qubits, params
 
 
-def simulate(circuit, init=None, gates=None) -> np.ndarray:
+def simulate(circuit, init=None, gates=None, omp: bool = True) -> np.ndarray:
     """Run the circuit from |0...0> (or from `init`, copied) and return the
-    final state vector (complex128, logical order)."""
+    final state vector (complex128, logical order).  omp=False runs the
+    single-threaded build."""
     n = circuit.n
     gl = circuit.gates if gates is None else gates
     if init is None:
@@ -81,7 +98,7 @@ def simulate(circuit, init=None, gates=None) -> np.ndarray:
         psi = np.array(init, dtype=np.complex128, copy=True)
         zero = 0
     kinds, qubits, params = encode(gl)
-    rc = lib().oracle_simulate(psi.ctypes.data, n, len(gl), kinds.ctypes.data,
+    rc = lib(omp).oracle_simulate(psi.ctypes.data, n, len(gl), kinds.ctypes.data,
                                qubits.ctypes.data, params.ctypes.data, zero)
     if rc != 0:
         raise RuntimeError(f"oracle_simulate failed rc={rc}")

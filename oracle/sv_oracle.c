@@ -120,8 +120,13 @@ int oracle_apply_gate(double *psi, int n, int kind, const int *q, const double *
   }
   cplx *s = (cplx *)psi;
   const uint64_t N = 1ULL << n;
-  cplx v[8], w[8];
+  /* The iterations touch disjoint amplitude groups, so the OpenMP build
+   * (liboracle_omp.so, -fopenmp) splits them over the host cores; every
+   * amplitude gets the same arithmetic in the same order as in the 1-thread
+   * build (bit-identical results). */
+#pragma omp parallel for schedule(static)
   for (uint64_t i = 0; i < N; i++) {
+    cplx v[8], w[8];
     if (i & mask) continue;
     for (int c = 0; c < d; c++) v[c] = s[i + off[c]];
     for (int r = 0; r < d; r++) {
@@ -151,6 +156,14 @@ int oracle_simulate(double *psi, int n, int m, const int *kinds, const int *qubi
   }
   return 0;
 }
+
+/* Threads the OpenMP build uses (1 in the plain build). */
+#ifdef _OPENMP
+#include <omp.h>
+int oracle_threads(void) { return omp_get_max_threads(); }
+#else
+int oracle_threads(void) { return 1; }
+#endif
 
 /* Squared norm sum |alpha_i|^2, for the norm-preservation pin. */
 double oracle_norm2(const double *psi, int n) {
