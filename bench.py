@@ -145,25 +145,82 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU oracle
-def cpu_oracle_sample(circ, budget_s=12.0, max_gates=None):
-    """Time the oracle (as it stands) on the first g gates of the workload
-    at full n, single thread.  Returns (updates/s, g, seconds)."""
+def host_info():
+    """nproc, CPU model and RAM of the host the oracle runs on."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                info["ram_gb"] = round(int(ln.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return info
+
+
+def cpu_oracle_sample(circ, budget_s=12.0, max_gates=None, omp=True):
+    """Time the oracle (as it stands) on the first g gates of the workload at
+    full n (g sized to ~budget_s; all of them if they fit).  omp: the OpenMP
+    build on every host core, else the 1-thread build.  Returns (updates/s,
+    g, seconds)."""
     from oracle import sim as O
-    import numpy as np
     n = circ.n
-    g = 1
-    # calibrate on one gate
+    # calibrate on one gate (includes the |0> init, so an upper bound)
     t0 = time.perf_counter()
-    O.simulate(C.Circuit(n, circ.gates[:1]))
-    t1 = time.perf_counter() - t0
-    per_gate = max(t1 * 0.8, 1e-6)  # includes the |0> init, so an upper bound
+    O.simulate(C.Circuit(n, circ.gates[:1]), omp=omp)
+    per_gate = max((time.perf_counter() - t0) * 0.8, 1e-7)
     g = max(1, min(len(circ.gates), int(budget_s / per_gate)))
     if max_gates:
         g = min(g, max_gates)
     t0 = time.perf_counter()
-    O.simulate(C.Circuit(n, circ.gates[:g]))
+    O.simulate(C.Circuit(n, circ.gates[:g]), omp=omp)
     dt = time.perf_counter() - t0
     return g * (2.0 ** n) / dt, g, dt
+
+
+def cpu_baseline(fam, n_full, budget_s=10.0):
+    """The oracle on the host cores: full circuits of
+    the workload's family at n = 12, 20, 24 on 1 core and on all cores
+    (n = 24 on 1 core: a leading-gate sample), and the workload itself at
+    n_full on all cores as a leading-gate sample (labelled extrapolation:
+    rate x whole circuit).  Returns the cpu_baseline object; its value is
+    the all-cores rate at the workload size."""
+    from oracle import sim as O
+    O.build()
+    nthr = O.threads(True)
+    rows = []
+    for n in (12, 20, 24):
+        c = C.make(fam, n)
+        for omp in (False, True):
+            if n == 24 and not omp:
+                v, g, dt = cpu_oracle_sample(c, budget_s=budget_s / 2, omp=False)
+            else:
+                t0 = time.perf_counter()
+                O.simulate(c, omp=omp)
+                dt = time.perf_counter() - t0
+                g = len(c.gates)
+                v = g * 2.0 ** n / dt
+            rows.append({"n": n, "cores": nthr if omp else 1, "gates": g, "of": len(c.gates),
+                         "s": round(dt, 3), "amp_updates_per_s": v,
+                         "kind": "full circuit" if g == len(c.gates) else "leading-gate sample"})
+    c = C.make(fam, n_full)
+    v, g, dt = cpu_oracle_sample(c, budget_s=budget_s, omp=True)
+    est = len(c.gates) * 2.0 ** n_full / v
+    rows.append({"n": n_full, "cores": nthr, "gates": g, "of": len(c.gates), "s": round(dt, 3),
+                 "amp_updates_per_s": v, "kind": "leading-gate sample",
+                 "extrapolated_full_circuit_s": round(est, 1)})
+    return {"value": v, "unit": "amp-updates/s", "cores": nthr, "kind": "oracle",
+            "sample": f"first {g} of {len(c.gates)} gates of {fam} n={n_full} (complex128 "
+                      f"gate-at-a-time C oracle, OpenMP over {nthr} host threads, {dt:.1f} s); "
+                      f"full circuit extrapolated: {est:.0f} s (labelled extrapolation)",
+            "host": host_info(), "by_size": rows}
 
 
 def load_peaks():
@@ -184,16 +241,21 @@ def load_traffic():
 
 # ------------------------------------------------------------- reference
 def run_reference(args):
+    """The tier's reference arm: the oracle as it stands (OpenMP build, every
+    host core), each step the leading gates of the workload at full n, sized
+    so that warm-up + steps end within ~3 minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     circ, fam, n = workload(args.workload, args.gpus)
     from oracle import sim as O
     O.build()
+    nthr = O.threads(True)
+    budget = max(0.5, min(6.0, 150.0 / max(1, args.warmup + args.steps)))
     vals = []
     per = None
     for i in range(args.warmup + args.steps):
-        v, g, dt = cpu_oracle_sample(circ, budget_s=6.0, max_gates=per)
+        v, g, dt = cpu_oracle_sample(circ, budget_s=budget, max_gates=per)
         per = g
         if i >= args.warmup:
             vals.append((v, dt))
@@ -203,12 +265,14 @@ def run_reference(args):
         "impl": "reference", "metric": "amplitude-updates/s (circuit simulation)",
         "value": value, "unit": "amp-updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{fam}_n{n}_fp64", "n": n, "gates": len(circ.gates),
                    "sample_gates_per_step": per},
-        "cpu_baseline": {"value": value, "unit": "amp-updates/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": "amp-updates/s", "cores": nthr, "kind": "oracle",
                          "sample": f"first {per} of {len(circ.gates)} gates of {fam} n={n} "
-                                   f"(complex128, gate-at-a-time C oracle) per step"},
+                                   f"(complex128, gate-at-a-time C oracle, OpenMP over {nthr} "
+                                   f"host threads) per step", "host": host_info()},
         "e2e": {"value": value, "unit": "amp-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -364,10 +428,7 @@ def run_atlas(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, g, dt = cpu_oracle_sample(circ, budget_s=12.0)
-        cpu = {"value": v, "unit": "amp-updates/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {g} of {m} gates of {fam} n={n} at full size, "
-                         f"complex128 gate-at-a-time C oracle, 1 thread, {dt:.1f} s"}
+        cpu = cpu_baseline(fam, n)
     sim.close()
     if rank != 0:
         if dist is not None:

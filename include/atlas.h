@@ -205,6 +205,10 @@ const char *atlas_last_error(void);
  *   "shm_ctas"       plan-specialised kernels of 2^12-amplitude fp64 tiles:
  *                    resident CTAs per SM, 2 (128 registers) or 3 (80
  *                    registers, when their shared memory fits) [2]
+ *   "shm_grid"       > 0: launch every shared-memory kernel on at most this
+ *                    many CTAs (each then loops over many tiles; parity
+ *                    tests exercise the multi-tile pipeline at small n);
+ *                    0 = the occupancy-derived grid [0]
  *   "shm_jit"        1 = each shared-memory launch runs a kernel generated
  *                    from its lowered op program and compiled with NVRTC for
  *                    sm_100a at the first atlas_run after a plan (cached per

@@ -118,7 +118,8 @@ struct ShmLaunch {
   // lowest tile bits, so the lanes of a warp cover contiguous 512-B runs.
   // lcol[b] = physical offset of tile bit b under the last phase's folded
   // map (1 << act[b] when it is the identity), lc0 = offset of its constant.
-  int32_t last_direct, pad;
+  int32_t last_direct;
+  int32_t grid_cap;            // > 0: at most this many CTAs (option shm_grid; tests)
   uint64_t lcol[16];
   uint64_t lc0;
 };

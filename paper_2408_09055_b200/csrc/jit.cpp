@@ -422,7 +422,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     os = oj + (size_t)jmasks.size() * NT * 4;
     ob = (os + (size_t)smaps.size() * NT * 2 + 15) & ~(size_t)15;
     om = ob + (size_t)nbt * 256 * 8;
-    off_bfac = (om + 3 * 8 + 15) & ~(size_t)15;
+    off_bfac = (om + 6 * 8 + 15) & ~(size_t)15;
     off_tfac = off_bfac + (size_t)4 * NB * esz;
     return off_tfac + (size_t)NTF * NT * esz;  // bfac: [group][parity][slot]
   };
@@ -431,13 +431,22 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   // threads, named barriers) sharing a ring of three tile buffers: a tile's
   // load is issued into the buffer the other group just finished with, so up
   // to two loads are in flight while both groups compute; completion is
-  // tracked by cp.async -> mbarrier arrivals
+  // tracked by cp.async -> mbarrier arrivals.  The k-th tile of the CTA
+  // (buffer k % 3) completes on mbarrier k % 6, not k % 3: consecutive
+  // phases of one mbarrier then belong to tiles of the SAME group (k and
+  // k + 6), so a group never waits on phase j + 1 of a barrier whose phase j
+  // (the other group's tile) is still in flight -- with k % 3, a parity wait
+  // for phase j + 1 succeeds while phase j is incomplete (try_wait.parity
+  // only distinguishes the current phase from the preceding one), which let
+  // a fast group read a buffer before its load landed (round-1 qsvm n=28
+  // mirror, |a0 - 1| = 2e-6).
   // (two groups of 256: the fp64 2^12 tiles; fp32's 2 x 512 threads at 64
   // registers measured slower than two single-buffer CTAs)
   bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 512 &&
               layout(3, off_jtab, off_stab, off_btab, off_mbar) + 1024 <= 233472;
   // the thread-factor table must not cost occupancy (or exceed the opt-in
   // limit): drop slots until it fits beside the resident CTAs
+  if (pipe) minb = 1;
   if (NTF) {
     const int keep = NTF;
     NTF = 0;
@@ -450,7 +459,6 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   }
   const size_t smem = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar);
   const int BT = pipe ? 2 * NT : NT;  // threads per CTA
-  if (pipe) minb = 1;
   // option shm_ctas = 3: three resident CTAs per SM (register cap 80) when
   // their shared memory fits the SM
   if (minb == 2 && C->opt.shm_ctas >= 3 && 3 * (smem + 1024) <= 233472) minb = 3;
@@ -490,7 +498,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   if (pipe) {
     o << "  const int tid = threadIdx.x & " << NT - 1 << ", grp = threadIdx.x / " << NT << ";\n";
     o << "  const unsigned mbar0 = (unsigned)__cvta_generic_to_shared(smraw + " << off_mbar << ");\n";
-    o << "  if (threadIdx.x == 0) for (int i = 0; i < 3; i++) asm volatile(\"mbarrier.init.shared::cta.b64 "
+    o << "  if (threadIdx.x == 0) for (int i = 0; i < 6; i++) asm volatile(\"mbarrier.init.shared::cta.b64 "
          "[%0], %1;\" :: \"r\"(mbar0 + 8 * i), \"r\"(" << NT << ") : \"memory\");\n";
   } else {
     o << "  const int tid = threadIdx.x;\n";
@@ -574,7 +582,7 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
       if ((it >> i) & 1) x |= 1ull << sl.act[K - RB + i];
     itoff[it] = x;
   }
-  o << "  auto issue_load = [&](int bsel, u64 base) {\n    const T *g = st + base + off_t;\n";
+  o << "  auto issue_load = [&](int bsel, " << (pipe ? "int msel, " : "") << "u64 base) {\n    const T *g = st + base + off_t;\n";
   for (int it = 0; it < NE; it++) {
     o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (sw_tid ^ "
       << swz(it * NT) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
@@ -582,13 +590,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
     else o << "asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
   }
   if (pipe)
-    o << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(mbar0 + 8 * bsel) : \"memory\");\n  };\n";
+    o << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(mbar0 + 8 * msel) : \"memory\");\n  };\n";
   else
     o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n  };\n";
   // pipe, zero mode: the ring protocol without data (plain arrivals)
   if (pipe)
-    o << "  auto issue = [&](int bsel, u64 base) { if (!zmode) issue_load(bsel, base); else asm volatile("
-         "\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mbar0 + 8 * bsel) : \"memory\"); };\n";
+    o << "  auto issue = [&](int bsel, int msel, u64 base) { if (!zmode) issue_load(bsel, msel, base); else asm volatile("
+         "\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mbar0 + 8 * msel) : \"memory\"); };\n";
   const std::string GS = pipe ? "gsync(grp);" : "__syncthreads();";
 
   const int last = sl.nphase - 1;
@@ -614,13 +622,13 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   const bool early = nbuf == 1;
   const std::string NTL = u64lit(sl.ntiles);
   const std::string next_issue =
-      pipe ? "{ const u64 nx = blockIdx.x + (i + 3) * G; if (nx < " + NTL + ") issue(b, tile_base(nx)); }"
+      pipe ? "{ const u64 nx = blockIdx.x + (u64)(i + 3) * G; if (nx < " + NTL + ") issue(b, mb < 3 ? mb + 3 : mb - 3, tile_base(nx)); }"
            : "if (!zmode) { const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
   if (pipe) {
     // tiles i = 0, 1, 2 of this CTA's sequence into buffers 0, 1, 2, each
     // issued by the group that will process it (i & 1)
     o << "  for (int i = grp; i < 3; i += 2) { const u64 t = blockIdx.x + (u64)i * G; if (t < " << NTL
-      << ") issue(i, tile_base(t)); }\n";
+      << ") issue(i, i, tile_base(t)); }\n";
   } else if (early) {
     o << "  if (!zmode) issue_load(0, tile_base(tile));\n";
   } else {
@@ -629,11 +637,12 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
         << ") issue_load(" << k << ", tile_base(t)); else asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\"); }\n";
   }
   if (pipe) {
-    o << "  for (u64 i = grp;; i += 2) {\n";
-    o << "    const u64 tile = blockIdx.x + i * G;\n    if (tile >= " << NTL << ") break;\n";
+    o << "  int mb = grp;  // i % 6 (i: the CTA's tile counter; mbarrier of tile i)\n";
+    o << "  for (unsigned i = grp;; i += 2, mb = mb >= 4 ? mb - 4 : mb + 2) {\n";
+    o << "    const u64 tile = blockIdx.x + (u64)i * G;\n    if (tile >= " << NTL << ") break;\n";
     o << "    const u64 base = tile_base(tile);\n";
-    o << "    const int b = (int)(i % 3);\n";
-    o << "    mbar_wait(mbar0 + 8 * b, (unsigned)((i / 3) & 1));\n";
+    o << "    const int b = mb < 3 ? mb : mb - 3;\n";
+    o << "    mbar_wait(mbar0 + 8 * mb, (i / 6) & 1);\n";
   } else {
   o << "  int b = 0;\n";
   o << "  for (; tile < " << NTL << "; tile += G) {\n";
@@ -1161,6 +1170,7 @@ cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_
   }
   uint64_t grid = (uint64_t)g_nsms * E->nt;
   if (grid > sl.ntiles) grid = sl.ntiles;
+  if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
   void *args[] = {&st, &zmode};
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);

@@ -723,6 +723,7 @@ static cudaError_t launch_shm_k(void *st, const ShmLaunch &sl, const ShmOp *ops,
   if (occ < 1) occ = 1;
   uint64_t grid = (uint64_t)num_sms() * occ;
   if (grid > sl.ntiles) grid = sl.ntiles;
+  if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
   kern<<<(unsigned)grid, NT, lay.total, s>>>((T *)st, sl, ops, coef, ph, ents, terms);
   return cudaGetLastError();
 }

@@ -334,15 +334,18 @@ void run(atlas_ctx *C) {
         mark(ln.type, zm ? ln.bytes / 2 : ln.bytes);
         switch (ln.type) {
           case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
-          case L_SHM:
+          case L_SHM: {
+            ShmLaunch sl = ln.sl;
+            sl.grid_cap = C->opt.shm_grid;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, ln.sl, C->stream, zm));
+              CK(launch_shm_jit(ln.jit, st, sl, C->stream, zm));
               break;
             }
-            CK(launch_shm(dt, st, ln.sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
+            CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                           (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
                           (const PermTerm *)C->d_terms, C->stream));
             break;
+          }
           case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;
           default: fail(ATLAS_E_INVALID, "internal: unexpected launch type %d", ln.type);
         }

@@ -189,7 +189,8 @@ def test_mirror_full_size(fam):
 
 @pytest.mark.parametrize("opt", [
     {"shm_direct_store": 0}, {"shm_explicit_perm": 1}, {"shm_rb": 3}, {"shm_nbuf": 2},
-    {"shm_nbuf": 3}, {"shm_direct_store": 0, "shm_explicit_perm": 1}, {"shm_ctas": 3}, {"shm_pipe": 1}])
+    {"shm_nbuf": 3}, {"shm_direct_store": 0, "shm_explicit_perm": 1}, {"shm_pipe": 0},
+    {"shm_pipe": 0, "shm_ctas": 3}])
 @pytest.mark.parametrize("fam", ["su2random", "qsvm", "random"])
 def test_shm_lowering_variants(fam, opt):
     """Every shared-memory lowering variant (direct last-phase store, explicit

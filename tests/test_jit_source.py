@@ -46,20 +46,25 @@ def ptxas(src, tmp_path, name):
     return regs, int(spill.group(1)) if spill else 0
 
 
-@pytest.mark.parametrize("fam,dtype", [("su2random", 0), ("qsvm", 0), ("qft", 1), ("random", 0)])
+@pytest.mark.parametrize("fam,dtype", [("su2random", 0), ("qsvm", 0), ("ising", 0), ("qft", 1),
+                                       ("su2random", 1), ("random", 0)])
 def test_jit_sources_compile_without_spills(fam, dtype, tmp_path):
+    """Every launch of the plan compiles within its launch bounds.  The
+    benchmark families (the kernels bench.py times) must not spill at all.
+    The all-kinds random circuit may spill a few words: its conditional
+    register permutations (X/CX/SWAP with thread/tile-dependent controls
+    that cannot be folded into addresses, OP_PERM1) keep two copies of 16
+    complex doubles live at the 128-register cap of the 512-thread pipe CTA;
+    it is a parity workload, not a bench one."""
     c = C.random_circuit(16, 160, 17) if fam == "random" else C.make(fam, 16)
     srcs = sources(c, dtype)
     assert srcs, "plan has no shared-memory kernel"
-    for i, src in enumerate(srcs[:3]):
+    for i, src in enumerate(srcs):
         m = re.search(r"__launch_bounds__\((\d+), (\d+)\)", src)
         threads, minb = int(m.group(1)), int(m.group(2))
         regs, spill = ptxas(src, tmp_path, f"k{i}")
         assert regs * threads * minb <= 65536
-        # at the register cap (128 for the 512-thread two-group CTA, 64 for
-        # fp32's 2 x 512 threads) a few bytes of spill around conditional
-        # diagonal factors are tolerated; more is a code-generation regression
-        assert spill <= (16 if dtype == 0 else 32), f"kernel {i} spills {spill} bytes"
+        assert spill <= (64 if fam == "random" else 0), f"kernel {i} spills {spill} bytes"
 
 
 def test_jit_source_reflects_program():
@@ -76,10 +81,18 @@ def test_jit_source_reflects_program():
     assert "switch" not in srcs[0]
 
 
-def test_jit_pipe_variant_compiles(tmp_path):
-    c = C.su2random(16)
-    srcs = sources(c, shm_pipe=1)
-    assert "mbarrier.try_wait.parity" in srcs[0]
-    m = re.search(r"__launch_bounds__\((\d+), (\d+)\)", srcs[0])
-    regs, spill = ptxas(srcs[0], tmp_path, "pipe")
-    assert regs * int(m.group(1)) <= 65536 and spill == 0
+@pytest.mark.parametrize("fam", ["su2random", "qsvm"])
+@pytest.mark.parametrize("pipe", [0, 1])
+def test_jit_pipe_variant_compiles(fam, pipe, tmp_path):
+    """Both pipelines on every launch: pipe mode (one CTA of two groups, six
+    mbarriers: tile i completes on barrier i % 6) and the two-CTA single
+    buffer (cp.async groups)."""
+    c = C.make(fam, 16)
+    srcs = sources(c, shm_pipe=pipe)
+    for i, src in enumerate(srcs):
+        assert ("mbarrier.try_wait.parity" in src) == bool(pipe)
+        if pipe:
+            assert "for (int i = 0; i < 6; i++)" in src and "mbar_wait(mbar0 + 8 * mb, (i / 6) & 1)" in src
+        m = re.search(r"__launch_bounds__\((\d+), (\d+)\)", src)
+        regs, spill = ptxas(src, tmp_path, f"p{i}")
+        assert regs * int(m.group(1)) * int(m.group(2)) <= 65536 and spill == 0
