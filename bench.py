@@ -55,13 +55,16 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--opt", action="append", default=[], help="extra library option key=int")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: n = workload n + log2 N (28 local qubits per GPU, the "
+                        "paper's E1); strong: n fixed (BASELINE config 4: n = 33 at N = 1/2/4/8)")
     return p.parse_args()
 
 
-def workload(name, world):
+def workload(name, world, scaling="weak"):
     fam, nstr = name.rsplit("_n", 1)
     n = int(nstr)
-    if world > 1:
+    if world > 1 and scaling == "weak":
         n += int(math.log2(world))  # weak scaling: 28 local qubits per GPU
     return C.make(fam, n), fam, n
 
@@ -247,7 +250,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    circ, fam, n = workload(args.workload, args.gpus)
+    circ, fam, n = workload(args.workload, args.gpus, args.scaling)
     from oracle import sim as O
     O.build()
     nthr = O.threads(True)
@@ -297,7 +300,7 @@ def run_atlas(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    circ, fam, n = workload(args.workload, world)
+    circ, fam, n = workload(args.workload, world, args.scaling)
     dtype = A.C128 if args.dtype == "f64" else A.C64
     uid = None
     if world > 1:
@@ -442,7 +445,7 @@ def run_atlas(args):
         "metric": "amplitude-updates/s (circuit simulation)",
         "value": value, "unit": "amp-updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": args.scaling, "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": f"{fam}_n{n}_{'fp64' if dtype == A.C128 else 'fp32'}",
                    "n": n, "gates": m, "L": stats["L"], "G": stats["G"],
