@@ -159,7 +159,9 @@ const char *atlas_last_error(void);
  *                    3 = front packing alone
  *   "front"          consider the front packing inside Kernelize [1]
  *   "dp_budget"      Kernelize DP state budget; beyond it the DP is abandoned
- *                    for the cheaper of the other candidates [1000000];
+ *                    for the cheaper of the other candidates [250000];
+ *                    states whose closed kernels already cost more than
+ *                    that cheaper candidate are dropped (branch and bound);
  *                    <= 0: no budget.  Deterministic (same on every rank).
  *   "prune_T"        Kernelize pruning threshold T [500];
  *                    <= 0 means no pruning
@@ -205,6 +207,12 @@ const char *atlas_last_error(void);
  *   "shm_ctas"       plan-specialised kernels of 2^12-amplitude fp64 tiles:
  *                    resident CTAs per SM, 2 (128 registers) or 3 (80
  *                    registers, when their shared memory fits) [2]
+ *   "shm_const_pool" plan-specialised fp64 kernels read their gate
+ *                    coefficients from a __constant__ table (LDCU.128 into
+ *                    uniform registers, two per instruction) instead of
+ *                    literals materialised by UMOV pairs; ptxas hoists the
+ *                    loads out of the tile loop and spills at the
+ *                    128-register cap, so it is off by default [0]
  *   "shm_grid"       > 0: launch every shared-memory kernel on at most this
  *                    many CTAs (each then loops over many tiles; parity
  *                    tests exercise the multi-tile pipeline at small n);
@@ -250,13 +258,15 @@ atlas_status atlas_nccl_unique_id(void *out128);
  * full length (call with cap = 0 to size). */
 atlas_status atlas_get_plan_json(atlas_ctx *ctx, char *buf, size_t cap, size_t *len);
 
-/* Plan summary, int64 values in this order (count = min(cap, 13)):
+/* Plan summary, int64 values in this order (count = min(cap, 14)):
  *   0 stages  1 staging cost x1000  2 kernels  3 fusion kernels  4 shm kernels
  *   5 kernel cost total  6 remaps  7 plan time (us)  8 staging exact (1/0)
  *   9 L  10 G  11 device launches per run
  *   12 time (us) the first atlas_run after this plan spent generating,
  *      compiling (NVRTC) and loading the plan-specialised shared-memory
- *      kernels (option "shm_jit"; 0 before that run) */
+ *      kernels (option "shm_jit"; 0 before that run)
+ *   13 staging time (us) within 7 (0 when the staging of an identical
+ *      request was reused) */
 atlas_status atlas_plan_stats(atlas_ctx *ctx, int64_t *out, int cap);
 
 /* The CUDA source of the plan-specialised kernel of shared-memory launch

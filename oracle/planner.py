@@ -236,6 +236,80 @@ def ilp_enumerate(circuit, L: int, Gq: int, s: int, c: float = 3, facts=None):
     return best, opt
 
 
+def ilp_highs(circuit, L: int, Gq: int, s: int, c: float = 3, facts=None, time_limit=120.0):
+    """The paper's staging ILP, literally (objective Eq. P:L1491, constraints
+    c1, cdeft, c2, c3, c4, c5, cag, c6 at P:L1495-1502, F_{g,-1} = 0 per
+    reading R3), with R = n - L - G regional qubits, handed to an
+    off-the-shelf ILP solver as the paper does (it used PuLP +
+    HiGHS; here HiGHS through scipy.optimize.milp).  For instances far beyond
+    ``ilp_enumerate``.  Returns (objective or None if infeasible, optimal:
+    bool, A as s x n 0/1 list of local sets)."""
+    import numpy as np
+    from scipy.optimize import Bounds, LinearConstraint, milp
+    from scipy.sparse import lil_matrix
+    n = circuit.n
+    facts = facts if facts is not None else gate_facts(circuit)
+    m = len(facts)
+    edges = dependencies(facts)
+    # variable layout: A[q,k], B[q,k], F[g,k], S[q,k<s-1], T[q,k<s-1]
+    nA = n * s
+    oA, oB, oF = 0, nA, 2 * nA
+    oS = oF + m * s
+    oT = oS + n * (s - 1)
+    nv = oT + n * (s - 1)
+    A_ = lambda q, k: oA + q * s + k  # noqa: E731
+    B_ = lambda q, k: oB + q * s + k  # noqa: E731
+    F_ = lambda g, k: oF + g * s + k  # noqa: E731
+    S_ = lambda q, k: oS + q * (s - 1) + k  # noqa: E731
+    T_ = lambda q, k: oT + q * (s - 1) + k  # noqa: E731
+    cost = np.zeros(nv)
+    for q in range(n):
+        for k in range(s - 1):
+            cost[S_(q, k)] = 1.0
+            cost[T_(q, k)] = c
+    rows = []  # (coeffs dict, lo, hi)
+    for q in range(n):
+        for k in range(s - 1):
+            rows.append(({A_(q, k + 1): 1, A_(q, k): -1, S_(q, k): -1}, -np.inf, 0))   # c1
+            rows.append(({B_(q, k + 1): 1, B_(q, k): -1, T_(q, k): -1}, -np.inf, 0))   # cdeft
+    for g in range(m):
+        for k in range(s - 1):
+            rows.append(({F_(g, k): 1, F_(g, k + 1): -1}, -np.inf, 0))                  # c2
+        for q in facts[g][1]:
+            for k in range(s):
+                d = {F_(g, k): 1, A_(q, k): -1}
+                if k > 0:
+                    d[F_(g, k - 1)] = -1                                                # c3
+                rows.append((d, -np.inf, 0))
+        rows.append(({F_(g, s - 1): 1}, 1, 1))                                          # c5
+    for g1, g2 in edges:
+        for k in range(s):
+            rows.append(({F_(g1, k): 1, F_(g2, k): -1}, 0, np.inf))                     # c4
+    for q in range(n):
+        for k in range(s):
+            rows.append(({A_(q, k): 1, B_(q, k): 1}, -np.inf, 1))                       # cag
+    for k in range(s):
+        rows.append(({A_(q, k): 1 for q in range(n)}, L, L))                            # c6
+        rows.append(({B_(q, k): 1 for q in range(n)}, Gq, Gq))
+    M = lil_matrix((len(rows), nv))
+    lo = np.empty(len(rows))
+    hi = np.empty(len(rows))
+    for i, (d, a, b) in enumerate(rows):
+        for j, v in d.items():
+            M[i, j] = v
+        lo[i], hi[i] = a, b
+    res = milp(cost, constraints=LinearConstraint(M.tocsr(), lo, hi),
+               integrality=np.ones(nv), bounds=Bounds(0, 1),
+               options={"time_limit": time_limit, "disp": False})
+    if res.status == 2:  # infeasible
+        return None, True, None
+    if res.x is None:
+        return None, False, None
+    x = np.round(res.x).astype(int)
+    locs = [[q for q in range(n) if x[A_(q, k)]] for k in range(s)]
+    return float(round(res.fun, 9)), res.status == 0, locs
+
+
 # ----------------------------------------------------------------------------
 # kernel cost model (SPEC S:L245-253, P:L1958-1968)
 # ----------------------------------------------------------------------------

@@ -209,11 +209,11 @@ class Simulator:
         return json.loads(buf.value.decode())
 
     def plan_stats(self) -> dict:
-        v = (ctypes.c_int64 * 13)()
-        _check(lib().atlas_plan_stats(self._ctx, v, 13))
+        v = (ctypes.c_int64 * 14)()
+        _check(lib().atlas_plan_stats(self._ctx, v, 14))
         keys = ["stages", "staging_cost_x1000", "kernels", "fusion_kernels", "shm_kernels",
                 "kernel_cost", "remaps", "plan_us", "staging_exact", "L", "G",
-                "launches_per_run", "jit_us"]
+                "launches_per_run", "jit_us", "stage_us"]
         return dict(zip(keys, list(v)))
 
     def jit_source(self, index: int, slot: int = 0) -> str:

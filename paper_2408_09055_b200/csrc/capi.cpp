@@ -1,5 +1,9 @@
 // capi.cpp -- extern "C" entry points declared in include/atlas.h.
+#include <chrono>
 #include <cmath>
+#include <exception>
+#include <memory>
+#include <thread>
 #include <cstring>
 #include <new>
 
@@ -9,6 +13,7 @@ namespace atlas {
 const char *last_error_cstr();
 void build_plan(atlas_ctx *C, int s_max, double cf);
 std::string plan_json(const atlas_ctx *C);
+CostModel builtin_cost_model(atlas_dtype dt);
 void run(atlas_ctx *C);
 void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count);
 void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count);
@@ -20,10 +25,10 @@ std::string shm_jit_source_of(const atlas_ctx *C, int slot, int i);
 
 using namespace atlas;
 
-#define GUARD(body)                           \
+#define GUARD(...)                            \
   try {                                       \
     set_last_error("");                       \
-    body;                                     \
+    __VA_ARGS__;                              \
     return ATLAS_OK;                          \
   } catch (const Error &e) {                  \
     set_last_error(e.msg);                    \
@@ -100,43 +105,71 @@ atlas_status atlas_load_circuit(atlas_ctx *C, const atlas_gate *gates, size_t m)
     }
     C->gates.swap(v);
     C->planned = false;
+    C->sp_key_valid = false;
   })
 }
+
 
 atlas_status atlas_plan(atlas_ctx *C, int s_max, double c) {
   GUARD({
     need(C != nullptr, ATLAS_E_INVALID, "ctx is NULL");
     need(s_max >= 1, ATLAS_E_INVALID, "s_max must be >= 1");
     need(c >= 0 && std::isfinite(c), ATLAS_E_INVALID, "c must be finite and >= 0");
-    build_plan(C, s_max, c);
     // ls_qubits unset with the built-in model: also plan with one forced
     // least-significant qubit fewer (256-B runs stream as well as 512-B runs
     // on B200 HBM3e, and a tile then spans one more high qubit) and keep the
-    // plan of lower model cost (ties: the model's setting)
-    // contiguous runs stay >= 256 B (fp64: ls >= 4, fp32: ls >= 5); 128-B
-    // runs measured slower per pass (fp32 su2random n=28: 11.4 vs 11.0 ms)
+    // plan of lower model cost (ties: the model's setting); the two plans
+    // are built concurrently.  Contiguous runs stay >= 256 B (fp64: ls >= 4,
+    // fp32: ls >= 5); 128-B runs measured slower per pass (fp32 su2random
+    // n=28: 11.4 vs 11.0 ms)
     const int ls_min = C->dt == ATLAS_C128 ? 4 : 5;
-    if (C->opt.ls_qubits < 0 && C->opt.cost_model.empty() && C->opt.ls_auto &&
-        C->cm.ls_qubits - 1 >= ls_min) {
-      auto total = [&]() {
-        int64_t t = 0;
-        for (auto &kp : C->kplans) t += kp.total;
-        return t;
-      };
-      const double us0 = C->plan_us;
-      const int64_t ca = total();
-      const int la = C->cm.ls_qubits;
-      C->opt.ls_qubits = la - 1;
+    const int la = builtin_cost_model(C->dt).ls_qubits;
+    if (!(C->opt.ls_qubits < 0 && C->opt.cost_model.empty() && C->opt.ls_auto && la - 1 >= ls_min)) {
       build_plan(C, s_max, c);
-      double us = us0 + C->plan_us;
-      if (total() >= ca) {
-        C->opt.ls_qubits = la;
-        build_plan(C, s_max, c);
-        us += C->plan_us;
-      }
-      C->opt.ls_qubits = -1;
-      C->plan_us = us;
+      return ATLAS_OK;
     }
+    auto t0 = std::chrono::steady_clock::now();
+    std::unique_ptr<atlas_ctx> alt(new atlas_ctx(*C));
+    alt->opt.ls_qubits = la - 1;
+    std::exception_ptr ep;
+    std::thread th([&]() {
+      try {
+        build_plan(alt.get(), s_max, c);
+      } catch (...) {
+        ep = std::current_exception();
+      }
+    });
+    try {
+      build_plan(C, s_max, c);
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (ep) std::rethrow_exception(ep);
+    auto total = [](const atlas_ctx *X) {
+      int64_t t = 0;
+      for (auto &kp : X->kplans) t += kp.total;
+      return t;
+    };
+    if (total(alt.get()) < total(C)) {  // the model's setting wins ties
+      std::swap(alt->cm, C->cm);
+      std::swap(alt->maps, C->maps);
+      std::swap(alt->stage_gates, C->stage_gates);
+      std::swap(alt->kplans, C->kplans);
+      std::swap(alt->exch, C->exch);
+      std::swap(alt->K_tile, C->K_tile);
+      std::swap(alt->nslots, C->nslots);
+      std::swap(alt->prog, C->prog);
+      std::swap(alt->coef, C->coef);
+      std::swap(alt->ops, C->ops);
+      std::swap(alt->phases, C->phases);
+      std::swap(alt->ents, C->ents);
+      std::swap(alt->terms, C->terms);
+      std::swap(alt->mats, C->mats);
+      std::swap(alt->newpos, C->newpos);
+    }
+    C->plan_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
   })
 }
 
@@ -220,6 +253,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_tfac_min") { o.shm_tfac_min = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_pipe") { o.shm_pipe = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_ctas") { need(v == 2 || v == 3, ATLAS_E_INVALID, "shm_ctas is 2 or 3"); o.shm_ctas = (int)v; C->jit_ready = false; replan = false; }
+    else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_grid") { need(v >= 0, ATLAS_E_INVALID, "shm_grid >= 0"); o.shm_grid = (int)v; replan = false; }
     else if (k == "shm_jit") { o.shm_jit = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "dp_budget") o.dp_budget = (long long)v;
@@ -293,7 +327,7 @@ atlas_status atlas_plan_stats(atlas_ctx *C, int64_t *out, int cap) {
   GUARD({
     need(C != nullptr && out != nullptr, ATLAS_E_INVALID, "NULL argument");
     need(C->planned, ATLAS_E_ORDER, "no plan");
-    int64_t v[13] = {0};
+    int64_t v[14] = {0};
     v[0] = C->sp.s;
     v[1] = (int64_t)llround(C->sp.cost * 1000);
     for (auto &kp : C->kplans) {
@@ -315,7 +349,8 @@ atlas_status atlas_plan_stats(atlas_ctx *C, int64_t *out, int cap) {
       if (ln.type == L_FUSED || ln.type == L_SHM || ln.type == L_SCALE || ln.type == L_PACK) nl++;
     v[11] = nl;
     v[12] = (int64_t)C->jit_us;
-    for (int i = 0; i < cap && i < 13; i++) out[i] = v[i];
+    v[13] = (int64_t)C->stage_us;
+    for (int i = 0; i < cap && i < 14; i++) out[i] = v[i];
   })
 }
 

@@ -77,8 +77,9 @@ struct Options {
   int shm_pipe = 1;          // JIT: two thread groups per CTA on a ring of 3 tile buffers
   int shm_ctas = 2;          // JIT: resident SHM CTAs per SM for 2^12 fp64 tiles (2 or 3)
   int shm_grid = 0;          // > 0: cap every SHM launch at this many CTAs (tests: many tiles per CTA at small n)
+  int shm_const_pool = 0;    // JIT fp64: coefficients in a __constant__ table (c[] operands, no UMOV)
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter
-  long long dp_budget = 1000000;
+  long long dp_budget = 250000;
   std::string cost_model;
 };
 
@@ -99,9 +100,15 @@ struct atlas_ctx {
   // plan
   bool planned = false;
   double plan_us = 0;
+  double stage_us = 0;         // staging part of plan_us
   double c = 3;
   atlas::CostModel cm;
   atlas::StagePlan sp;
+  // key of the staging in sp (invalidated by atlas_load_circuit)
+  bool sp_key_valid = false;
+  int sp_key_smax = 0;
+  double sp_key_c = 0;
+  long sp_key_budget = 0;
   std::vector<atlas::StageMap> maps;
   std::vector<std::vector<int>> stage_gates;     // circuit ids per stage (order)
   std::vector<atlas::KernelPlan> kplans;         // per stage; gate ids = circuit ids

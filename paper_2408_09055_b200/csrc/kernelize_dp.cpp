@@ -404,8 +404,17 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
     }
     return best_plan;
   };
+  // branch and bound: the cheaper of the front packing and OrderedKernelize
+  // is computed first; a DP state whose closed kernels alone already cost
+  // more can never be returned (the DP result is taken only when <= it), so
+  // it is dropped.  If every state is dropped the DP cannot win.
+  const KernelPlan ub_plan = fallback();
+  const int64_t UB = getenv("ATLAS_DP_NOBOUND") ? INF64 : ub_plan.total;
   for (int i = 0; i < nu; i++) {
-    if (emitted > budget) return fallback();
+    if (emitted > budget) {
+      if (getenv("ATLAS_DEBUG")) fprintf(stderr, "[kernelize] units=%d budget out at %d ub=%lld\n", nu, i, (long long)UB);
+      return ub_plan;
+    }
     const Unit &u = units[i];
     if (!getenv("ATLAS_DP_NOFUT")) {
       C.fut_q = fq[i + 1];
@@ -430,6 +439,7 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
     auto emit = [&](St &&s) {
       emitted++;
       C.close_dead_prefix(s);
+      if (s.closed_cost > UB) return;
       if ((int)next.size() >= 8 * T && T < INT_MAX / 16) {
         // keep the working set bounded inside an iteration as well (same
         // criterion as the pruning of P:L2496)
@@ -670,7 +680,11 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
         merge_group(s4, (int)s4.ks.size() - 1);
       }
     }
-    if (next.empty()) fail(ATLAS_E_INFEASIBLE, "Kernelize: unit %d fits no kernel", i);
+    if (next.empty()) {
+      if (getenv("ATLAS_DEBUG")) fprintf(stderr, "[kernelize] units=%d bounded out at %d emitted %lld\n", nu, i, (long long)emitted);
+      if (UB < INF64) return ub_plan;  // every state is bounded out
+      fail(ATLAS_E_INFEASIBLE, "Kernelize: unit %d fits no kernel", i);
+    }
     if (getenv("ATLAS_DEBUG_DP"))
     {
       size_t tot = 0, mx = 0;
@@ -742,7 +756,7 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
   // the cheapest valid candidate: the DP, OrderedKernelize (Thm. dp-optimal
   // guarantees DP <= Ordered without pruning; pruning may worsen
   // it) and the commutation-aware front packing (R29)
-  KernelPlan best_plan = fallback();
+  KernelPlan best_plan = ub_plan;
   if (valid && kp.total <= best_plan.total) best_plan = kp;
   return best_plan;
 }

@@ -17,9 +17,12 @@
 // relabelling: it toggles the qubit's flip bit (R14); the factor of
 // Y-like gates becomes a per-rank scalar (R15).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <sstream>
 #include <tuple>
@@ -264,7 +267,19 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
   for (int g = 0; g < m; g++) C->info[g] = classify(C->gates[g]);
   // ---- a2: staging
   C->c = cf;
-  C->sp = stage_circuit(n, L, G, C->info, s_max, cf, C->opt.stage_budget);
+  // the staging depends only on the circuit, L, G, s_max, c and the budget:
+  // reuse it when atlas_plan rebuilds the plan for another ls_qubits (ls_auto)
+  if (C->sp_key_valid && C->sp_key_smax == s_max && C->sp_key_c == cf &&
+      C->sp_key_budget == C->opt.stage_budget) {
+    // stage_us keeps the time of the staging that is reused
+  } else {
+    C->sp = stage_circuit(n, L, G, C->info, s_max, cf, C->opt.stage_budget);
+    C->stage_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    C->sp_key_valid = true;
+    C->sp_key_smax = s_max;
+    C->sp_key_c = cf;
+    C->sp_key_budget = C->opt.stage_budget;
+  }
   const int s = C->sp.s;
   C->stage_gates.assign(s, {});
   for (int g = 0; g < m; g++) C->stage_gates[C->sp.gate_stage[g]].push_back(g);
@@ -305,8 +320,23 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
   const int64_t pass_bytes = 2 * ((int64_t)B << L);
   auto slot_rank = [&](int sl) { return C->nslots > 1 ? sl : C->rank; };
 
+  // Three passes over the stages: (A) placement, remap launches and the
+  // insular specialisation (the next stage's mapping depends on the flips
+  // this produces, not on kernelization), (B) Kernelize of every stage on
+  // host threads (independent; each deterministic), (C) lowering.
+  struct StageWork {
+    std::vector<std::vector<Launch>> pre;   // pack / exchange launches per slot
+    std::vector<std::vector<LGate>> lg;
+    std::vector<cd> scalar;
+    std::vector<KGate> seq;
+    std::vector<int> seq_pos;
+    KernelizeOptions ko;
+    KernelPlan kp;
+  };
+  std::vector<StageWork> SW(s);
   for (int k = 0; k < s; k++) {
     StageMap &mp = C->maps[k];
+    SW[k].pre.assign(C->nslots, {});
     // ---- remap from stage k-1
     if (k > 0) {
       const StageMap &pm = C->maps[k - 1];
@@ -353,7 +383,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           ln.stage = k;
           ln.newpos_off = off;
           ln.bytes = pass_bytes;
-          C->prog[sl].push_back(ln);
+          SW[k].pre[sl].push_back(ln);
         }
         ex.packed = true;
         for (int q = 0; q < n; q++) at[sigma[q]] = q;
@@ -379,7 +409,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           ln.type = L_EXCHANGE;
           ln.stage = k;
           ln.bytes = (int64_t)(((double)(B) * (double)(1ull << L)) * (1.0 - std::ldexp(1.0, -gp)));
-          C->prog[sl].push_back(ln);
+          SW[k].pre[sl].push_back(ln);
         }
       mp.sigma = sigma;
       mp.flip_begin = flip;
@@ -387,10 +417,12 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
     // ---- insular specialisation, in circuit order, per simulated rank
     const std::vector<int> &ids = C->stage_gates[k];
     std::vector<int> flip = mp.flip_begin;
-    std::vector<std::vector<LGate>> lg(C->nslots, std::vector<LGate>(ids.size()));
-    std::vector<cd> scalar(C->nslots, cd(1));
-    std::vector<KGate> seq;
-    std::vector<int> seq_pos;  // position in ids
+    std::vector<std::vector<LGate>> &lg = SW[k].lg;
+    lg.assign(C->nslots, std::vector<LGate>(ids.size()));
+    std::vector<cd> &scalar = SW[k].scalar;
+    scalar.assign(C->nslots, cd(1));
+    std::vector<KGate> &seq = SW[k].seq;
+    std::vector<int> &seq_pos = SW[k].seq_pos;  // position in ids
     for (size_t ii = 0; ii < ids.size(); ii++) {
       const Gate &g = C->gates[ids[ii]];
       const GateInfo &gi = C->info[ids[ii]];
@@ -471,8 +503,8 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
       }
     }
     mp.flip_end = flip;
-    // ---- a3: kernelization of the stage
-    KernelizeOptions ko;
+    // ---- a3: kernelization options of the stage
+    KernelizeOptions &ko = SW[k].ko;
     ko.algo = C->opt.kernelizer;
     ko.prune_T = C->opt.prune_T;
     ko.lift = C->opt.lift != 0;
@@ -482,13 +514,46 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
     ko.dp_budget = C->opt.dp_budget;
     ko.L = L;
     ko.ls_set = ls_logical(mp.sigma, std::min(C->cm.ls_qubits, L));
-    KernelPlan kp;
-    if (!seq.empty()) {
-      if (ko.algo == 1) kp = ordered_kernelize(seq, C->cm, ko);
-      else if (ko.algo == 2) kp = greedy_kernelize(seq, C->cm, ko);
-      else if (ko.algo == 3) kp = front_kernelize(seq, C->cm, ko);
-      else kp = dp_kernelize(seq, C->cm, ko);
-    }
+  }
+  // ---- (B) a3: Kernelize every stage, stages spread over host threads
+  {
+    std::atomic<int> next{0};
+    std::vector<std::exception_ptr> errs(s);
+    auto worker = [&]() {
+      for (;;) {
+        const int k = next.fetch_add(1);
+        if (k >= s) return;
+        try {
+          StageWork &w = SW[k];
+          if (w.seq.empty()) continue;
+          if (w.ko.algo == 1) w.kp = ordered_kernelize(w.seq, C->cm, w.ko);
+          else if (w.ko.algo == 2) w.kp = greedy_kernelize(w.seq, C->cm, w.ko);
+          else if (w.ko.algo == 3) w.kp = front_kernelize(w.seq, C->cm, w.ko);
+          else w.kp = dp_kernelize(w.seq, C->cm, w.ko);
+        } catch (...) {
+          errs[k] = std::current_exception();
+        }
+      }
+    };
+    unsigned nth = std::thread::hardware_concurrency();
+    nth = std::max(1u, std::min<unsigned>(nth ? nth : 1, (unsigned)s));
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nth; t++) th.emplace_back(worker);
+    worker();
+    for (auto &t : th) t.join();
+    for (int k = 0; k < s; k++)
+      if (errs[k]) std::rethrow_exception(errs[k]);
+  }
+  // ---- (C) lowering
+  for (int k = 0; k < s; k++) {
+    StageMap &mp = C->maps[k];
+    for (int sl = 0; sl < C->nslots; sl++)
+      for (auto &ln : SW[k].pre[sl]) C->prog[sl].push_back(ln);
+    std::vector<std::vector<LGate>> &lg = SW[k].lg;
+    std::vector<cd> &scalar = SW[k].scalar;
+    std::vector<KGate> &seq = SW[k].seq;
+    std::vector<int> &seq_pos = SW[k].seq_pos;
+    const KernelPlan &kp = SW[k].kp;
     // kernel gate indices are positions in seq; keep them for lowering and
     // translate to circuit ids for the plan report
     C->kplans[k] = kp;

@@ -25,6 +25,9 @@
 //    the best states (most gates executed, then cost) and the plan is marked
 //    exact = false (reported in the plan JSON and DESIGN.md).
 #include <algorithm>
+#include <functional>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 
@@ -34,63 +37,27 @@ namespace atlas {
 
 namespace {
 
-struct Frontier {
-  std::vector<u64> w;
-  bool operator==(const Frontier &o) const { return w == o.w; }
-};
+typedef std::vector<u64> Frontier;
 
-struct StateKey {
-  u64 h;
-  u64 g;
-  bool operator==(const StateKey &o) const { return h == o.h && g == o.g; }
-};
-struct KeyHash {
-  size_t operator()(const StateKey &k) const { return (size_t)(k.h * 0x9E3779B97F4A7C15ull ^ k.g); }
-};
-
-struct State {
-  Frontier f;
-  u64 g;
-  double cost;
-  std::vector<u64> prefix;
-  int ndone;
-};
-
-struct Ctx {
-  int n, L, G, m;
-  const std::vector<GateInfo> *info;
-  std::vector<std::vector<int>> preds;
-  long evals = 0;
-
-  bool done(const Frontier &f, int g) const { return (f.w[g >> 6] >> (g & 63)) & 1; }
-  void set(Frontier &f, int g) const { f.w[g >> 6] |= 1ull << (g & 63); }
-
-  // maximal execution of one stage with local set `loc` (c3, c4)
-  int maxexec(Frontier &f, u64 loc) {
-    evals++;
-    int added = 0;
-    for (int g = 0; g < m; g++) {
-      if (done(f, g)) continue;
-      if ((*info)[g].nonins & ~loc) continue;
-      bool ok = true;
-      for (int p : preds[g])
-        if (!done(f, p)) { ok = false; break; }
-      if (ok) { set(f, g); added++; }
-    }
-    return added;
-  }
-  u64 remaining_nonins(const Frontier &f) const {
-    u64 u = 0;
-    for (int g = 0; g < m; g++)
-      if (!done(f, g)) u |= (*info)[g].nonins;
-    return u;
-  }
-  u64 hash(const Frontier &f) const {
+struct FHash {
+  size_t operator()(const Frontier &f) const {
     u64 h = 1469598103934665603ull;
-    for (u64 x : f.w) { h ^= x; h *= 1099511628211ull; h ^= h >> 29; }
-    return h;
+    for (u64 x : f) { h ^= x; h *= 1099511628211ull; h ^= h >> 29; }
+    return (size_t)h;
   }
 };
+
+bool subset(const Frontier &a, const Frontier &b) {  // a ⊆ b
+  for (size_t i = 0; i < a.size(); i++)
+    if (a[i] & ~b[i]) return false;
+  return true;
+}
+
+int fcount(const Frontier &f) {
+  int c = 0;
+  for (u64 x : f) c += popc(x);
+  return c;
+}
 
 u64 full_mask(int n) { return n == 64 ? ~0ull : ((1ull << n) - 1); }
 
@@ -108,9 +75,141 @@ u64 final_global(u64 prev, u64 allowed, int G) {
   return need == 0 ? g : ~0ull;
 }
 
-bool better(double c1, const std::vector<u64> &p1, double c2, const std::vector<u64> &p2) {
-  if (c1 != c2) return c1 < c2;
-  return p1 < p2;
+// all subsets of `pool` with exactly k bits, ascending as integers
+void combos(u64 pool, int k, std::vector<u64> &out) {
+  out.clear();
+  std::vector<int> bits;
+  for (u64 p = pool; p; p &= p - 1) bits.push_back(ctz(p));
+  const int nb = (int)bits.size();
+  if (k > nb || k < 0) return;
+  if (k == 0) {
+    out.push_back(0);
+    return;
+  }
+  std::vector<int> idx(k);
+  for (int i = 0; i < k; i++) idx[i] = i;
+  for (;;) {
+    u64 v = 0;
+    for (int i = 0; i < k; i++) v |= 1ull << bits[idx[i]];
+    out.push_back(v);
+    int i = k - 1;
+    while (i >= 0 && idx[i] == nb - k + i) i--;
+    if (i < 0) break;
+    idx[i]++;
+    for (int j = i + 1; j < k; j++) idx[j] = idx[j - 1] + 1;
+  }
+  std::sort(out.begin(), out.end());
+}
+
+struct Search {
+  int n, L, G, m, words;
+  u64 all;
+  const std::vector<GateInfo> *info;
+  std::vector<std::vector<int>> preds, succs;
+  long evals = 0;
+  long budget;
+  bool over = false;
+  bool dbg = getenv("ATLAS_DEBUG_STAGE") != nullptr;
+  // scratch of levels()
+  std::vector<int> lv;
+  std::vector<u64> lw;
+
+  bool done(const Frontier &f, int g) const { return (f[g >> 6] >> (g & 63)) & 1; }
+
+  // maximal execution of one stage with local set `loc` (c3, c4): one pass in
+  // circuit order reaches the fixpoint, since every predecessor comes earlier
+  int maxexec(Frontier &f, u64 loc) {
+    evals++;
+    int added = 0;
+    for (int g = 0; g < m; g++) {
+      if (done(f, g)) continue;
+      if ((*info)[g].nonins & ~loc) continue;
+      bool ok = true;
+      for (int p : preds[g])
+        if (!done(f, p)) { ok = false; break; }
+      if (ok) { f[g >> 6] |= 1ull << (g & 63); added++; }
+    }
+    return added;
+  }
+  u64 remaining_nonins(const Frontier &f) const {
+    u64 u = 0;
+    for (int g = 0; g < m; g++)
+      if (!done(f, g)) u |= (*info)[g].nonins;
+    return u;
+  }
+
+  // Stage levels of the remaining gates (lower bounds, exact reasoning):
+  // forward h(g) = earliest stage (0 = the next one) any plan can run g in.
+  // With H = max h over g's pending predecessors, every pending ancestor a
+  // of g with h(a) = H runs no earlier than H and no later than g, so if g
+  // ran at H all of them would share that stage and the union W of their
+  // non-insular qubits would have to be local: |W| > L forces h(g) = H + 1.
+  // Backward b(g) = stages any plan needs after g's stage, by the mirror
+  // argument over descendants.  Returns the lower bound on the number of
+  // stages that finish every pending gate (a virtual sink after all of
+  // them); fills fwd (h) and bwd (b) per gate (-1 = done).
+  int levels(const Frontier &f, std::vector<int> &fwd, std::vector<int> &bwd) {
+    fwd.assign(m, -1);
+    bwd.assign(m, -1);
+    lw.assign(m, 0);
+    int top = -1;
+    for (int g = 0; g < m; g++) {
+      if (done(f, g)) continue;
+      int H = 0;
+      for (int p : preds[g])
+        if (!done(f, p)) H = std::max(H, fwd[p]);
+      u64 W = (*info)[g].nonins;
+      for (int p : preds[g])
+        if (!done(f, p) && fwd[p] == H) W |= lw[p];
+      if (popc(W) > L) { H++; W = (*info)[g].nonins; }
+      fwd[g] = H;
+      lw[g] = W;
+      top = std::max(top, H);
+    }
+    if (top < 0) return 0;
+    u64 Ws = 0;
+    for (int g = 0; g < m; g++)
+      if (fwd[g] == top) Ws |= lw[g];
+    const int lb = popc(Ws) > L ? top + 2 : top + 1;
+    lw.assign(m, 0);
+    for (int g = m - 1; g >= 0; g--) {
+      if (done(f, g)) continue;
+      int B = 0;
+      for (int q : succs[g]) B = std::max(B, bwd[q]);
+      u64 V = (*info)[g].nonins;
+      for (int q : succs[g])
+        if (bwd[q] == B) V |= lw[q];
+      if (popc(V) > L) { B++; V = (*info)[g].nonins; }
+      bwd[g] = B;
+      lw[g] = V;
+    }
+    return lb;
+  }
+};
+
+struct MemoKey {
+  Frontier f;
+  u64 g;
+  int k;
+  bool operator==(const MemoKey &o) const { return g == o.g && k == o.k && f == o.f; }
+};
+struct MemoHash {
+  size_t operator()(const MemoKey &x) const {
+    return FHash()(x.f) ^ (size_t)(x.g * 0x9E3779B97F4A7C15ull) ^ (size_t)x.k;
+  }
+};
+
+// global set of the next stage for a chosen constrained part: keep the
+// free previous globals (cost 0; the lowest ones if there are more than the
+// free slots), then the lowest other free qubits -- free qubits are
+// interchangeable for every later stage, so this is the cheapest and then
+// lexicographically smallest completion (R5)
+u64 fill_free(u64 c, u64 prev, u64 freeq, int G) {
+  int need = G - popc(c);
+  u64 g = c;
+  for (u64 p = prev & freeq; p && need > 0; p &= p - 1) { g |= p & (~p + 1); need--; }
+  for (u64 p = freeq & ~g; p && need > 0; p &= p - 1) { g |= p & (~p + 1); need--; }
+  return need == 0 ? g : ~0ull;
 }
 
 }  // namespace
@@ -124,56 +223,11 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
            popc(info[g].nonins), L);
   StagePlan sp;
   const u64 all = full_mask(n);
-  if (G == 0 || m == 0) {
-    // with no global qubit every gate is local: one stage, cost 0
-    u64 g0 = 0;
-    if (G > 0) {
-      u64 u = 0;
-      for (auto &x : info) u |= x.nonins;
-      g0 = final_global(0, all & ~u, G);
-    }
-    sp.s = 1;
-    sp.local = {all & ~g0};
-    sp.global = {g0};
-    sp.gate_stage.assign(m, 0);
-    return sp;
-  }
-  Ctx C{n, L, G, m, &info, {}, 0};
-  C.preds.resize(m);
   {
-    std::vector<int> last(n, -1);
-    for (int g = 0; g < m; g++) {
-      u64 q = info[g].qmask;
-      while (q) {
-        int b = ctz(q);
-        q &= q - 1;
-        if (last[b] >= 0 &&
-            std::find(C.preds[g].begin(), C.preds[g].end(), last[b]) == C.preds[g].end())
-          C.preds[g].push_back(last[b]);  // edge set E: adjacent pairs
-        last[b] = g;
-      }
-    }
-  }
-  // candidate global sets in increasing bitmask order (Gosper)
-  std::vector<u64> cand;
-  {
-    u64 v = (1ull << G) - 1;
-    while (v <= all && v != 0) {
-      cand.push_back(v);
-      u64 t = v | (v - 1);
-      if (t == ~0ull) break;
-      v = (t + 1) | (((~t & -~t) - 1) >> (ctz(v) + 1));
-    }
-  }
-  const int words = (m + 63) / 64;
-  const double unit = 1.0 + c;
-  bool exact = true;
-
-  // s = 1
-  {
+    // one stage: the global set avoids every non-insular qubit (cost 0)
     u64 u = 0;
     for (auto &x : info) u |= x.nonins;
-    u64 g0 = final_global(0, all & ~u, G);
+    const u64 g0 = G == 0 ? 0 : final_global(0, all & ~u, G);
     if (g0 != ~0ull) {
       sp.s = 1;
       sp.local = {all & ~g0};
@@ -182,100 +236,171 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
       return sp;
     }
   }
-  // layer 0
-  std::vector<State> layer;
+  Search S;
+  S.n = n; S.L = L; S.G = G; S.m = m; S.words = (m + 63) / 64; S.all = all;
+  S.info = &info; S.budget = std::max(1000L, budget);
+  S.preds.resize(m);
+  S.succs.resize(m);
   {
-    std::unordered_map<StateKey, int, KeyHash> idx;
-    for (u64 g0 : cand) {
-      Frontier f{std::vector<u64>(words, 0)};
-      int a = C.maxexec(f, all & ~g0);
-      if (a == 0) continue;
-      StateKey k{C.hash(f), g0};
-      if (idx.count(k)) continue;
-      idx[k] = (int)layer.size();
-      layer.push_back(State{f, g0, 0.0, {g0}, a});
+    std::vector<int> last(n, -1);
+    for (int g = 0; g < m; g++) {
+      u64 q = info[g].qmask;
+      while (q) {
+        int b = ctz(q);
+        q &= q - 1;
+        if (last[b] >= 0 &&
+            std::find(S.preds[g].begin(), S.preds[g].end(), last[b]) == S.preds[g].end()) {
+          S.preds[g].push_back(last[b]);  // edge set E: adjacent pairs
+          S.succs[last[b]].push_back(g);
+        }
+        last[b] = g;
+      }
     }
   }
-  for (int s = 2; s <= s_max; s++) {
-    // completion in one more stage?
-    int best = -1;
-    double best_cost = 0;
-    std::vector<u64> best_pref;
-    for (int i = 0; i < (int)layer.size(); i++) {
-      const State &st = layer[i];
-      u64 u = C.remaining_nonins(st.f);
-      u64 gl = final_global(st.g, all & ~u, G);
-      if (gl == ~0ull) continue;
-      double cost = st.cost + unit * popc(gl & ~st.g);
-      std::vector<u64> pref = st.prefix;
-      pref.push_back(gl);
-      if (best < 0 || better(cost, pref, best_cost, best_pref)) {
-        best = i;
-        best_cost = cost;
-        best_pref = pref;
-      }
+  const double unit = 1.0 + c;
+  const Frontier empty(S.words, 0);
+  // Depth-first branch and bound over the per-stage global sets, in
+  // increasing bitmask order (so among plans of equal cost the first found
+  // is the canonical one, R5), for s = the level lower bound,
+  // s + 1, ...  (Thm. ilp-optimal: the minimum s first; then the
+  // minimum objective Eq. P:L1477).  Every pruning is exact:
+  //  * viability: the stage-level bound of the remaining gates must fit the
+  //    stages left;
+  //  * cost bound: cost so far + unit * (current globals that some remaining
+  //    gate forces local at the next stage + for every later boundary the
+  //    globals that cannot avoid such a gate) >= the best plan found;
+  //  * transpositions: a (frontier, global set, stage) reached again at no
+  //    lower cost (a later, lexicographically larger prefix);
+  //  * global sets differ only in their constrained part (qubits with
+  //    remaining non-insular gates); the free qubits are completed by
+  //    fill_free.
+  std::vector<int> fwd, bwd;
+  std::vector<u64> cons_sets;
+  bool exact = true;
+  int sfound = -1;
+  double best_cost = 1e300;
+  std::vector<u64> best_pref;
+  auto lower_cost = [&](int s, int k, u64 g, const std::vector<int> &fw, const std::vector<int> &bw) {
+    // k = index of the stage just executed with global set g
+    std::vector<u64> F(s + 1, 0);  // F[j]: qubits forced local at stage j+1 if global at j
+    for (int x = 0; x < m; x++) {
+      if (fw[x] < 0) continue;
+      const int e = k + 1 + fw[x], lat = s - 1 - bw[x];
+      const u64 nq = info[x].nonins;
+      if (lat <= k + 1) F[k] |= nq;
+      for (int j = k + 1; j <= s - 2; j++)
+        if (e >= j && lat <= j + 1) F[j] |= nq;
     }
-    if (best >= 0) {
-      sp.s = s;
-      sp.cost = best_cost;
-      sp.exact = exact;
-      sp.global = best_pref;
-      for (u64 g : sp.global) sp.local.push_back(all & ~g);
-      // replay maximal execution to assign gate stages
-      Frontier f{std::vector<u64>(words, 0)};
-      sp.gate_stage.assign(m, -1);
-      for (int k = 0; k < s; k++) {
-        Frontier before = f;
-        C.maxexec(f, sp.local[k]);
-        for (int g = 0; g < m; g++)
-          if (C.done(f, g) && !C.done(before, g)) sp.gate_stage[g] = k;
+    double lb = popc(g & F[k]);
+    for (int j = k + 1; j <= s - 2; j++) lb += std::max(0, G - (n - popc(F[j])));
+    return unit * lb;
+  };
+  for (int s = 2; s <= s_max && sfound < 0; s++) {
+    const int lb0 = S.levels(empty, fwd, bwd);
+    if (lb0 > s) continue;
+    std::unordered_map<MemoKey, double, MemoHash> memo;
+    std::vector<u64> pref;
+    bool stop = false;
+    double root_lb = 1e300;
+    // node: stage k executed with global set g, frontier f, cost so far
+    std::function<void(int, const Frontier &, u64, double)> dfs = [&](int k, const Frontier &f, u64 g, double cost) {
+      if (stop) return;
+      if (k == s - 2) {
+        const u64 gl = final_global(g, all & ~S.remaining_nonins(f), G);
+        if (gl == ~0ull) return;
+        const double tot = cost + unit * popc(gl & ~g);
+        if (tot < best_cost) {
+          best_cost = tot;
+          best_pref = pref;
+          best_pref.push_back(gl);
+          if (S.dbg) fprintf(stderr, "  s=%d plan cost %g evals %ld\n", s, tot, S.evals);
+          if (best_cost <= root_lb) stop = true;
+        }
+        return;
       }
-      for (int g = 0; g < m; g++)
-        if (sp.gate_stage[g] < 0) fail(ATLAS_E_INFEASIBLE, "internal: staging replay incomplete");
-      sp.states_explored = C.evals;
-      return sp;
-    }
-    if (s == s_max) break;
-    // expand to the next layer
-    std::vector<State> next;
-    std::unordered_map<StateKey, int, KeyHash> idx;
-    long projected = (long)layer.size() * (long)cand.size();
-    if (projected > budget) {
-      // keep the states that executed the most gates (then cheapest, then lexicographic)
-      std::sort(layer.begin(), layer.end(), [](const State &a, const State &b) {
-        if (a.ndone != b.ndone) return a.ndone > b.ndone;
-        if (a.cost != b.cost) return a.cost < b.cost;
-        return a.prefix < b.prefix;
-      });
-      size_t keep = std::max<size_t>(1, (size_t)(budget / (long)cand.size()));
-      if (layer.size() > keep) {
-        layer.resize(keep);
-        exact = false;
-      }
-    }
-    for (const State &st : layer) {
-      for (u64 g : cand) {
-        Frontier f = st.f;
-        int a = C.maxexec(f, all & ~g);
-        if (a == 0) continue;
-        double cost = st.cost + unit * popc(g & ~st.g);
-        StateKey k{C.hash(f), g};
-        auto it = idx.find(k);
-        std::vector<u64> pref = st.prefix;
-        pref.push_back(g);
-        if (it == idx.end()) {
-          idx[k] = (int)next.size();
-          next.push_back(State{f, g, cost, pref, st.ndone + a});
-        } else if (better(cost, pref, next[it->second].cost, next[it->second].prefix)) {
-          next[it->second].cost = cost;
-          next[it->second].prefix = pref;
+      const u64 cons = S.remaining_nonins(f);
+      const u64 freeq = all & ~cons;
+      const int kmin = std::max(0, G - popc(freeq));
+      std::vector<u64> cand;
+      for (int kk = kmin; kk <= std::min(G, popc(cons)); kk++) {
+        combos(cons, kk, cons_sets);
+        for (u64 cc : cons_sets) {
+          const u64 g2 = fill_free(cc, k < 0 ? 0 : g, freeq, G);
+          if (g2 == ~0ull) continue;
+          // more constrained globals than needed: when every newly global
+          // one could be replaced by an unused free previous global (no
+          // swap) the replacement is strictly cheaper and executes a superset
+          const int newc = popc(cc & ~g);
+          if (kk > kmin && k >= 0 && newc > 0 && newc <= popc(g & freeq & ~g2)) continue;
+          cand.push_back(g2);
         }
       }
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      std::vector<int> fw, bw;
+      for (u64 g2 : cand) {
+        if (stop) return;
+        if (S.evals > S.budget) { S.over = true; stop = true; return; }
+        Frontier f2 = f;
+        if (S.maxexec(f2, all & ~g2) == 0) continue;
+        const double c2 = k < 0 ? 0.0 : cost + unit * popc(g2 & ~g);
+        const int need = S.levels(f2, fw, bw);
+        if (need > s - 1 - (k + 1)) continue;
+        if (c2 + lower_cost(s, k + 1, g2, fw, bw) >= best_cost) continue;
+        MemoKey key{f2, g2, k + 1};
+        auto it = memo.find(key);
+        if (it != memo.end() && it->second <= c2) continue;
+        memo[key] = c2;
+        pref.push_back(g2);
+        dfs(k + 1, f2, g2, c2);
+        pref.pop_back();
+      }
+    };
+    // the cost bound at the root: every boundary's unavoidable swaps
+    {
+      std::vector<int> fw0, bw0;
+      S.levels(empty, fw0, bw0);
+      double lb = 0;
+      for (int j = 0; j <= s - 2; j++) {
+        u64 Fj = 0;
+        for (int x = 0; x < m; x++) {
+          const int e = fw0[x], lat = s - 1 - bw0[x];
+          if (e >= j && lat <= j + 1) Fj |= info[x].nonins;
+        }
+        lb += std::max(0, G - (n - popc(Fj)));
+      }
+      root_lb = unit * lb;
     }
-    layer.swap(next);
-    if (layer.empty()) break;
+    dfs(-1, empty, 0, 0.0);
+    if (!best_pref.empty()) sfound = s;
+    if (S.over) exact = false;
+    if (S.dbg) fprintf(stderr, "s=%d found=%d cost %g root_lb %g evals %ld over %d\n", s, sfound, best_cost, root_lb, S.evals, (int)S.over);
+    if (S.over && sfound < 0) {
+      // budget exhausted without a plan at this s: look further (not exact)
+      S.over = false;
+      S.evals = 0;
+    }
   }
-  fail(ATLAS_E_INFEASIBLE, "no staging with at most %d stages", s_max);
+  if (sfound < 0) fail(ATLAS_E_INFEASIBLE, "no staging with at most %d stages", s_max);
+  const int sstar = sfound;
+  sp.s = sstar;
+  sp.cost = best_cost;
+  sp.exact = exact;
+  sp.global = best_pref;
+  for (u64 g : sp.global) sp.local.push_back(all & ~g);
+  // replay maximal execution to assign gate stages
+  Frontier f = empty;
+  sp.gate_stage.assign(m, -1);
+  for (int k = 0; k < sstar; k++) {
+    Frontier before = f;
+    S.maxexec(f, sp.local[k]);
+    for (int g = 0; g < m; g++)
+      if (S.done(f, g) && !S.done(before, g)) sp.gate_stage[g] = k;
+  }
+  for (int g = 0; g < m; g++)
+    if (sp.gate_stage[g] < 0) fail(ATLAS_E_INFEASIBLE, "internal: staging replay incomplete");
+  sp.states_explored = S.evals;
+  return sp;
 }
 
 }  // namespace atlas
