@@ -213,6 +213,11 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
+ *   "shm_fuse_pack"  the local bit permutation ("pack") that precedes a
+ *                    remap's exchange is folded into the store addresses of
+ *                    the previous stage's last shared-memory launch, which
+ *                    then writes to the other buffer (no standalone pack
+ *                    pass) [1]
  *   "shm_grid"       > 0: launch every shared-memory kernel on at most this
  *                    many CTAs (each then loops over many tiles; parity
  *                    tests exercise the multi-tile pipeline at small n);

@@ -254,6 +254,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_pipe") { o.shm_pipe = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_ctas") { need(v == 2 || v == 3, ATLAS_E_INVALID, "shm_ctas is 2 or 3"); o.shm_ctas = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
+    else if (k == "shm_fuse_pack") o.shm_fuse_pack = (int)v;
     else if (k == "shm_grid") { need(v >= 0, ATLAS_E_INVALID, "shm_grid >= 0"); o.shm_grid = (int)v; replan = false; }
     else if (k == "shm_jit") { o.shm_jit = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "dp_budget") o.dp_budget = (long long)v;

@@ -76,6 +76,7 @@ struct Options {
   int shm_tfac_min = 4;      // JIT: thread-only factor tables for slots with >= this many entries (0: off)
   int shm_pipe = 1;          // JIT: two thread groups per CTA on a ring of 3 tile buffers
   int shm_ctas = 2;          // JIT: resident SHM CTAs per SM for 2^12 fp64 tiles (2 or 3)
+  int shm_fuse_pack = 1;     // the remap pack fused into the previous stage's last SHM launch
   int shm_grid = 0;          // > 0: cap every SHM launch at this many CTAs (tests: many tiles per CTA at small n)
   int shm_const_pool = 0;    // JIT fp64: coefficients in a __constant__ table (c[] operands, no UMOV)
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter

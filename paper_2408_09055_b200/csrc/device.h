@@ -122,6 +122,11 @@ struct ShmLaunch {
   int32_t grid_cap;            // > 0: at most this many CTAs (option shm_grid; tests)
   uint64_t lcol[16];
   uint64_t lc0;
+  // >= 0: the fused remap pack (plan.cpp, option shm_fuse_pack): offset of
+  // the L-entry slot map in the newpos blob; the launch then writes to the
+  // other buffer with local slot b moved to newpos[b] (plan-specialised
+  // kernels only; the interpreter runs in place and a permute follows)
+  int64_t out_perm_off;
 };
 
 // Fused dense kernel ("Fusion"): one 2^k x 2^k matrix on k slots.

@@ -231,6 +231,22 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   const ShmPhase *ph = C->phases.data() + sl.phase_off;
   const DiagEnt *ents = C->ents.data() + sl.ent_off;
   const PermTerm *terms = C->terms.data() + sl.term_off;
+  // fused remap pack (plan.cpp): the launch writes its output to the other
+  // buffer with every local slot b moved to slot np[b] -- the bit
+  // permutation of the pack that precedes the next stage's exchange
+  // (P:L1312 Shard).  P() maps an output offset; being a bit permutation it
+  // distributes over the XOR / OR of disjoint offsets, so every store-side
+  // constant is mapped at generation time and the tile base by a table.
+  const bool operm = sl.out_perm_off >= 0;
+  std::vector<int> np;
+  if (operm) np.assign(C->newpos.begin() + sl.out_perm_off, C->newpos.begin() + sl.out_perm_off + C->L);
+  auto PB = [&](uint64_t x) {
+    if (!operm) return x;
+    uint64_t r = 0;
+    for (int b = 0; b < (int)np.size(); b++)
+      if ((x >> b) & 1) r |= 1ull << np[b];
+    return r;
+  };
   int minb = (nbuf == 1 && (K - RB) >= 8 && (K - RB) <= 9 && (esz << K) <= 65536) ? 2 : 1;
 
   // ---- shared-memory swizzles per phase boundary and lanes per phase.
@@ -477,7 +493,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     oj = (size_t)ntile_bufs * TILE * esz;
     os = oj + (size_t)jmasks.size() * NT * 4;
     ob = (os + (size_t)smaps.size() * NT * 2 + 15) & ~(size_t)15;
-    om = ob + (size_t)nbt * 256 * 8;
+    om = ob + (size_t)nbt * 256 * 8 * (operm ? 2 : 1);
     off_bfac = (om + 6 * 8 + 15) & ~(size_t)15;
     off_tfac = off_bfac + (size_t)4 * NB * esz;
     return off_tfac + (size_t)NTF * NT * esz;  // bfac: [group][parity][slot]
@@ -544,7 +560,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
          "%0, 1, 0, p; }\" : \"=r\"(ok) : \"r\"(a), \"r\"(par) : \"memory\"); } while (!ok); }\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
-    << "(T *__restrict__ st, int zmode) {\n";
+    << "(T *__restrict__ st, T *dst, int zmode) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
@@ -563,6 +579,13 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "  for (int i = threadIdx.x; i < " << nbt * 256 << "; i += " << BT << ") { const int c = i >> 8; u64 m = "
     << u64lit(sl.nonactive) << "; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
     << "pdep64((u64)(i & 255), m); }\n";
+  if (operm) {
+    o << "  u64 *obtab = btab + " << nbt * 256 << ";\n";
+    o << "  for (int i = threadIdx.x; i < " << nbt * 256 << "; i += " << BT << ") { const u64 x = btab[i]; u64 r = 0;";
+    for (int b = 0; b < (int)np.size(); b++)
+      if (sl.nonactive >> b & 1) o << " r |= ((x >> " << b << ") & 1ull) << " << np[b] << ";";
+    o << " obtab[i] = r; }\n";
+  }
   // per-thread tile indices of every distinct (register mask, lane order):
   // thread bit i -> tile bit order[i] (kernels.cu shm_kernel prologue)
   auto thread_order = [&](int key) {
@@ -619,6 +642,10 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // this thread's HBM offset inside a tile
   o << "  u64 off_t = 0;";
   for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) off_t |= " << u64lit(1ull << sl.act[i]) << ";";
+  if (operm) {
+    o << "\n  u64 ooff_t = 0;";
+    for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) ooff_t |= " << u64lit(PB(1ull << sl.act[i])) << ";";
+  }
   o << "\n  const int sw_tid = swz(tid);\n";
   // copy-out reads the layout of the last boundary
   const Swz &SO = swzs[ssw[lastp]];
@@ -630,6 +657,11 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255]";
   for (int c = 1; c < nbt; c++) o << " | btab[" << 256 * c << " + ((tile >> " << 8 * c << ") & 255)]";
   o << "; };\n";
+  if (operm) {
+    o << "  auto otile_base = [&](u64 tile) { return obtab[tile & 255]";
+    for (int c = 1; c < nbt; c++) o << " | obtab[" << 256 * c << " + ((tile >> " << 8 * c << ") & 255)]";
+    o << "; };\n";
+  }
   // per-register-element offsets (constant)
   std::vector<uint64_t> itoff(NE);
   for (int it = 0; it < NE; it++) {
@@ -660,7 +692,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   if (ld) {
     o << "  u64 gthr = 0;\n  { const int jtl = (int)(jtab[" << jslot[last] * NT << " + tid] & 0xffffu);";
     for (int b = 0; b < K; b++)
-      if (sl.lcol[b]) o << " if ((jtl >> " << b << ") & 1) gthr ^= " << u64lit(sl.lcol[b]) << ";";
+      if (sl.lcol[b]) o << " if ((jtl >> " << b << ") & 1) gthr ^= " << u64lit(PB(sl.lcol[b])) << ";";
     o << " }\n";
   }
   if (pipe) {
@@ -697,12 +729,14 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "  for (unsigned i = grp;; i += 2, mb = mb >= 4 ? mb - 4 : mb + 2) {\n";
     o << "    const u64 tile = blockIdx.x + (u64)i * G;\n    if (tile >= " << NTL << ") break;\n";
     o << "    const u64 base = tile_base(tile);\n";
+    if (operm) o << "    const u64 obase = otile_base(tile);\n";
     o << "    const int b = mb < 3 ? mb : mb - 3;\n";
     o << "    mbar_wait(mbar0 + 8 * mb, (i / 6) & 1);\n";
   } else {
   o << "  int b = 0;\n";
   o << "  for (; tile < " << NTL << "; tile += G) {\n";
   o << "    const u64 base = tile_base(tile);\n";
+  if (operm) o << "    const u64 obase = otile_base(tile);\n";
   const int nwarps = BT / 32;
   for (auto &kv : bslot) {
     const int bk = kv.second;
@@ -1029,16 +1063,16 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       for (int i = 0; i < RB; i++) limg[i] = sl.lcol[P.rbit[i]];
       o << "      u64 cg = gthr;\n";
       if (P.permuted) {
-        o << "      cg ^= " << u64lit(sl.lc0) << ";\n";
+        o << "      cg ^= " << u64lit(PB(sl.lc0)) << ";\n";
         for (int i = P.term_begin; i < P.term_end; i++)
           o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
-            << ") cg ^= " << u64lit(terms[i].gvec) << ";\n";
+            << ") cg ^= " << u64lit(PB(terms[i].gvec)) << ";\n";
       }
       for (int e = 0; e < NE; e++) {
         uint64_t x = 0;
         for (int i = 0; i < RB; i++)
           if ((e >> i) & 1) x ^= limg[i];
-        o << "      st[base | (cg ^ " << u64lit(x) << ")] = v[" << e << "];\n";
+        o << "      " << (operm ? "dst[obase" : "st[base") << " | (cg ^ " << u64lit(PB(x)) << ")] = v[" << e << "];\n";
       }
       o << "    }\n";
       break;
@@ -1067,14 +1101,14 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "      " << GS << "\n    }\n";
   }
   if (!ld) {
-    o << "    { T *g = st + base + off_t;\n";
+    o << (operm ? "    { T *g = dst + obase + ooff_t;\n" : "    { T *g = st + base + off_t;\n");
     if (early) {
       for (int it = 0; it < NE; it++) o << "      v[" << it << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
       o << "      " << GS << "\n      " << next_issue << "\n";
-      for (int it = 0; it < NE; it++) o << "      g[" << u64lit(itoff[it]) << "] = v[" << it << "];\n";
+      for (int it = 0; it < NE; it++) o << "      g[" << u64lit(PB(itoff[it])) << "] = v[" << it << "];\n";
     } else {
       for (int it = 0; it < NE; it++)
-        o << "      g[" << u64lit(itoff[it]) << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
+        o << "      g[" << u64lit(PB(itoff[it])) << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
     }
     o << "    }\n";
   }
@@ -1205,7 +1239,7 @@ static int g_nsms = 0;
 
 bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->zero_ok; }
 
-cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s, int zmode) {
+cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode) {
   JitEntry *E = (JitEntry *)jit;
   const int NT = E->threads > 0 ? E->threads : 1 << (sl.K - sl.RB);
   if (E->attr_set < E->smem) {
@@ -1227,7 +1261,7 @@ cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_
   uint64_t grid = (uint64_t)g_nsms * E->nt;
   if (grid > sl.ntiles) grid = sl.ntiles;
   if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
-  void *args[] = {&st, &zmode};
+  void *args[] = {&st, &dst, &zmode};
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);
 }

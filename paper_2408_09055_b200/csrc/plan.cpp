@@ -646,6 +646,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           std::vector<int> tile_of_slot(L, -1);
           for (int b = 0; b < K_; b++) tile_of_slot[act[b]] = b;
           ln.sl = ShmLaunch{};
+          ln.sl.out_perm_off = -1;
           ln.sl.K = K_;
           ln.sl.RB = RB;
           ln.sl.nbuf = (C->dt == ATLAS_C128 && K_ == 13) ? 1 : C->opt.shm_nbuf;
@@ -1258,6 +1259,19 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
         ln.bytes = pass_bytes;
         C->prog[sl].push_back(ln);
       }
+      // fuse the next remap's pack (a bit permutation of the local slots)
+      // into this stage's last shared-memory launch: it stores its output
+      // permuted into the other buffer, so the standalone pack pass
+      // (a full read + write of the shard) disappears (P:L1312 Shard,
+      // north_star (4))
+      if (C->opt.shm_fuse_pack && k + 1 < s && !SW[k + 1].pre[sl].empty() &&
+          SW[k + 1].pre[sl][0].type == L_PACK && !C->prog[sl].empty() &&
+          C->prog[sl].back().type == L_SHM && C->prog[sl].back().stage == k) {
+        Launch &last = C->prog[sl].back();
+        last.sl.out_perm_off = SW[k + 1].pre[sl][0].newpos_off;
+        last.newpos_off = last.sl.out_perm_off;
+        SW[k + 1].pre[sl].erase(SW[k + 1].pre[sl].begin());
+      }
     }
   }
   C->planned = true;
@@ -1301,12 +1315,19 @@ std::string plan_json(const atlas_ctx *C) {
     o << "],\"flip_end\":[";
     for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].flip_end[q];
     o << "],\"packed\":" << (k > 0 && C->exch[k].packed ? "true" : "false");
-    o << ",\"pack_newpos\":";
+    o << ",\"pack_fused\":";
     {
       int64_t off = -1;
+      bool fused = false;
       if (!C->prog.empty())
-        for (const Launch &ln : C->prog[0])
+        for (const Launch &ln : C->prog[0]) {
           if (ln.stage == k && ln.type == L_PACK) off = ln.newpos_off;
+          if (ln.stage == k - 1 && ln.type == L_SHM && ln.newpos_off >= 0) {
+            off = ln.newpos_off;
+            fused = true;
+          }
+        }
+      o << (fused ? "true" : "false") << ",\"pack_newpos\":";
       if (off < 0) {
         o << "null";
       } else {

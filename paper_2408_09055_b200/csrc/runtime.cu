@@ -31,7 +31,7 @@ cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const in
 cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
 void shm_jit_prepare(atlas_ctx *C);
-cudaError_t launch_shm_jit(void *jit, void *st, const ShmLaunch &sl, cudaStream_t s, int zmode);
+cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode);
 bool shm_jit_zero_ok(const void *jit);
 
 #define CK(x)                                                                              \
@@ -337,13 +337,20 @@ void run(atlas_ctx *C) {
           case L_SHM: {
             ShmLaunch sl = ln.sl;
             sl.grid_cap = C->opt.shm_grid;
+            // a fused remap pack writes the permuted output to the other buffer
+            const bool operm = sl.out_perm_off >= 0;
+            void *dst = operm ? other_buf(C, s) : st;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, sl, C->stream, zm));
-              break;
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm));
+            } else {
+              CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
+                            (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
+                            (const PermTerm *)C->d_terms, C->stream));
+              if (operm)  // the interpreter runs in place; the pack follows
+                CK(launch_permute(dt, st, dst, C->L, &C->newpos[sl.out_perm_off],
+                                  (const int *)C->d_newpos + sl.out_perm_off, C->stream));
             }
-            CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
-                          (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
-                          (const PermTerm *)C->d_terms, C->stream));
+            if (operm) C->cur[s] ^= 1;
             break;
           }
           case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;

@@ -131,3 +131,27 @@ def test_qsvm_n28_mirror_repeated():
             assert abs(a0 - 1) <= 1e-10, f"run {rep}: |a0-1|={abs(a0 - 1):.3e}"
             rest = np.array([s.get_state(i, 1)[0] for i in idx])
             assert np.abs(rest).max() <= 1e-10
+
+
+@pytest.mark.parametrize("opt", [{"shm_fuse_pack": 0}, {"shm_jit": 0}, {"shm_grid": 2}])
+@pytest.mark.parametrize("W", [2, 8])
+def test_fused_pack_variants(W, opt):
+    """The remap pack fused into the previous stage's last shared-memory
+    launch (default) against the standalone pack (shm_fuse_pack = 0), the
+    interpreter's in-place-then-permute fallback (shm_jit = 0) and a capped
+    grid, su2random n = 20 (4 remaps, packs at W >= 2)."""
+    c = C.su2random(20)
+    (psi,), _ = run(c, world=W, **opt)
+    check(psi, O.simulate(c))
+
+
+def test_fused_pack_present():
+    """su2random at W = 8 needs packs; with fusion every one of them rides
+    on a shared-memory launch (no standalone pack launch)."""
+    c = C.su2random(20)
+    with A.Simulator(c.n, 0, 8, 0, virtual_world=1) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        pj = s.plan_json()
+    packed = [st for st in pj["stages"] if st["packed"]]
+    assert packed and all(st["pack_fused"] for st in packed)
