@@ -102,7 +102,9 @@ typedef struct {
 /* ---------------------------------------------------------------- core */
 
 /* Create a context for an n-qubit state sharded over `world` ranks (a power
- * of two, 1..64); this process is `rank`.  G = log2(world) global qubits,
+ * of two, 1..1024; beyond one 8-GPU box this serves planning studies such as
+ * PAPER.md's staging comparison at 31 qubits); this process is
+ * `rank`.  G = log2(world) global qubits,
  * L = n - G local qubits, R = 0.
  * nccl_uid: 128-byte ncclUniqueId from atlas_nccl_unique_id() on rank 0,
  * broadcast to all ranks; NULL when world == 1 or in virtual-world mode
@@ -156,7 +158,8 @@ const char *atlas_last_error(void);
  *                    DP, OrderedKernelize and the front packing (DESIGN.md
  *                    R29); 1 = OrderedKernelize; 2 = greedy fusion
  *                    packing up to 5 qubits (the paper's baseline);
- *                    3 = front packing alone
+ *                    3 = front packing alone; 4 = the Kernelize DP alone
+ *                    (pruning threshold T, no budget or fallback: E7)
  *   "front"          consider the front packing inside Kernelize [1]
  *   "dp_budget"      Kernelize DP state budget; beyond it the DP is abandoned
  *                    for the cheaper of the other candidates [250000];
@@ -233,6 +236,16 @@ const char *atlas_last_error(void);
  *                    later dense op needs their bits (else folded) [0]
  *   "device"         CUDA device ordinal [current device]
  *   "stage_budget"   staging search state budget [2000000]
+ *   "regional"       R: of the log2(world) rank bits, R count as regional
+ *                    qubits and the rest as global in the staging objective
+ *                    (Eq. P:L1491: newly local + c * newly global; Def.
+ *                    P:L1405-1417).  On one NVSwitch box the data movement
+ *                    is the same all-to-all either way; R > 0 emulates a
+ *                    two-tier interconnect so that c changes plans
+ *                    (R7) [0]
+ *   "stager"         0 = exact staging (the ILP optimum);
+ *                    1 = the SnuQS greedy heuristic (the paper's staging
+ *                    baseline; R32) [0]
  * String options:
  *   "cost_model"     path of a cost-model JSON (SPEC S:L358 format, integer
  *                    units); default: the built-in B200 fp64/fp32 model

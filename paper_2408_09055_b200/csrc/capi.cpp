@@ -55,8 +55,8 @@ atlas_status atlas_create(int n, atlas_dtype dtype, int world, int rank, const v
     need(out != nullptr, ATLAS_E_INVALID, "out is NULL");
     *out = nullptr;
     need(n >= 1 && n <= 48, ATLAS_E_INVALID, "n must be in [1, 48]");
-    need(world >= 1 && world <= 64 && (world & (world - 1)) == 0, ATLAS_E_INVALID,
-         "world must be a power of two in [1, 64]");
+    need(world >= 1 && world <= 1024 && (world & (world - 1)) == 0, ATLAS_E_INVALID,
+         "world must be a power of two in [1, 1024]");
     need(rank >= 0 && rank < world, ATLAS_E_INVALID, "rank out of range");
     need(dtype == ATLAS_C128 || dtype == ATLAS_C64, ATLAS_E_UNSUPPORTED, "unknown dtype");
     int G = __builtin_ctz((unsigned)world);
@@ -226,7 +226,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     std::string k(key);
     Options &o = C->opt;
     bool replan = true;
-    if (k == "kernelizer") { need(v >= 0 && v <= 3, ATLAS_E_INVALID, "kernelizer in 0..3"); o.kernelizer = (int)v; }
+    if (k == "kernelizer") { need(v >= 0 && v <= 4, ATLAS_E_INVALID, "kernelizer in 0..4"); o.kernelizer = (int)v; }
     else if (k == "prune_T") o.prune_T = (int)v;
     else if (k == "ls_qubits") { need(v >= 0 && v <= 13, ATLAS_E_INVALID, "ls_qubits in 0..13"); o.ls_qubits = (int)v; }
     else if (k == "shm_qubits") o.shm_qubits = (int)v;
@@ -241,6 +241,10 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "timing") { o.timing = (int)v; replan = false; }
     else if (k == "device") { need(!C->dev_ready, ATLAS_E_ORDER, "device must be set before the first run"); o.device = (int)v; replan = false; }
     else if (k == "stage_budget") o.stage_budget = (long)v;
+    else if (k == "regional") {
+      need(v >= 0 && v <= C->G, ATLAS_E_INVALID, "regional in [0, log2(world)]");
+      o.regional = (int)v;
+    } else if (k == "stager") { need(v == 0 || v == 1, ATLAS_E_INVALID, "stager is 0 or 1"); o.stager = (int)v; }
     else if (k == "shm_direct_store") o.shm_direct_store = (int)v;
     else if (k == "shm_explicit_perm") o.shm_explicit_perm = (int)v;
     else if (k == "front") o.front = (int)v;

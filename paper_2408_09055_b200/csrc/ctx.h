@@ -64,6 +64,8 @@ struct Options {
   int timing = 0;
   int device = -1;
   long stage_budget = 2000000;
+  int regional = 0;          // rank bits counted as regional qubits in the staging cost (R > 0 emulation)
+  int stager = 0;            // 0: exact staging (ILP optimum); 1: SnuQS greedy baseline (E5)
   int shm_nbuf = 1;
   int shm_direct_store = 1;
   int shm_rb = 4;
@@ -110,6 +112,8 @@ struct atlas_ctx {
   int sp_key_smax = 0;
   double sp_key_c = 0;
   long sp_key_budget = 0;
+  int sp_key_stager = 0;
+  int sp_key_regional = 0;
   std::vector<atlas::StageMap> maps;
   std::vector<std::vector<int>> stage_gates;     // circuit ids per stage (order)
   std::vector<atlas::KernelPlan> kplans;         // per stage; gate ids = circuit ids

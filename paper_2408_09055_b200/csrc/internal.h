@@ -109,7 +109,7 @@ struct KernelPlan {
 };
 
 struct KernelizeOptions {
-  int algo = 0;            // 0 Kernelize, 1 Ordered, 2 greedy-5
+  int algo = 0;            // 0 Kernelize, 1 Ordered, 2 greedy-5, 3 front, 4 the DP alone
   int prune_T = 500;
   bool lift = true;
   bool attach = true;
@@ -121,7 +121,8 @@ struct KernelizeOptions {
 };
 
 StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info,
-                        int s_max, double c, long budget);
+                        int s_max, double c, long budget, int R = 0);
+StagePlan stage_greedy(int n, int L, int G, const std::vector<GateInfo> &info, int s_max, double c);
 
 KernelPlan ordered_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                              const KernelizeOptions &o);
@@ -131,6 +132,10 @@ KernelPlan front_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                            const KernelizeOptions &o);
 KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                         const KernelizeOptions &o);
+// the DP of Alg. Kernelize alone (pruning at T, no budget, no bound, no
+// fallback candidates): the planner-time / cost trade-off of E7
+KernelPlan dp_only_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
+                             const KernelizeOptions &o);
 // cost of a kernel made of these gates, best kind (fusion preferred on a tie)
 int64_t kernel_cost(const std::vector<KGate> &seq, const std::vector<int> &idx,
                     const CostModel &cm, const KernelizeOptions &o, int *kind);

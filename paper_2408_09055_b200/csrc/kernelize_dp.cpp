@@ -368,8 +368,24 @@ bool order_is_valid(const std::vector<KGate> &seq, const std::vector<int> &order
 
 }  // namespace
 
+namespace {
+KernelPlan dp_impl(const std::vector<KGate> &seq, const CostModel &cm, const KernelizeOptions &o,
+                   bool dp_only);
+}
+
 KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
                         const KernelizeOptions &o) {
+  return dp_impl(seq, cm, o, false);
+}
+
+KernelPlan dp_only_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
+                             const KernelizeOptions &o) {
+  return dp_impl(seq, cm, o, true);
+}
+
+namespace {
+KernelPlan dp_impl(const std::vector<KGate> &seq, const CostModel &cm, const KernelizeOptions &o,
+                   bool dp_only) {
   KernelPlan ordered = ordered_kernelize(seq, cm, o);
   if (getenv("ATLAS_DP_PARTNERS")) kMaxPartners = atoi(getenv("ATLAS_DP_PARTNERS"));
   if (getenv("ATLAS_DP_MERGES")) kMaxMergesPerGate = atoi(getenv("ATLAS_DP_MERGES"));
@@ -393,7 +409,7 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
   // DP would exceed it, Kernelize falls back to the cheaper of the front
   // packing and OrderedKernelize (R29)
   long long emitted = 0;
-  const long long budget = o.dp_budget > 0 ? o.dp_budget : LLONG_MAX;
+  const long long budget = (o.dp_budget > 0 && !dp_only) ? o.dp_budget : LLONG_MAX;
   auto fallback = [&]() {
     KernelPlan best_plan = ordered;
     if (o.front) {
@@ -408,8 +424,8 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
   // is computed first; a DP state whose closed kernels alone already cost
   // more can never be returned (the DP result is taken only when <= it), so
   // it is dropped.  If every state is dropped the DP cannot win.
-  const KernelPlan ub_plan = fallback();
-  const int64_t UB = getenv("ATLAS_DP_NOBOUND") ? INF64 : ub_plan.total;
+  const KernelPlan ub_plan = dp_only ? KernelPlan{} : fallback();
+  const int64_t UB = (getenv("ATLAS_DP_NOBOUND") || dp_only) ? INF64 : ub_plan.total;
   for (int i = 0; i < nu; i++) {
     if (emitted > budget) {
       if (getenv("ATLAS_DEBUG")) fprintf(stderr, "[kernelize] units=%d budget out at %d ub=%lld\n", nu, i, (long long)UB);
@@ -752,7 +768,7 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
     fprintf(stderr, "[kernelize] units=%d dp_cost=%lld kernels=%zu ordered=%lld (%zu) valid=%d arena=%zu\n",
             nu, (long long)kp.total, kp.kernels.size(), (long long)ordered.total,
             ordered.kernels.size(), (int)valid, C.arena.size());
-  if (getenv("ATLAS_DEBUG_KEEP")) return kp;
+  if (getenv("ATLAS_DEBUG_KEEP") || dp_only) return kp;
   // the cheapest valid candidate: the DP, OrderedKernelize (Thm. dp-optimal
   // guarantees DP <= Ordered without pruning; pruning may worsen
   // it) and the commutation-aware front packing (R29)
@@ -760,5 +776,7 @@ KernelPlan dp_kernelize(const std::vector<KGate> &seq, const CostModel &cm,
   if (valid && kp.total <= best_plan.total) best_plan = kp;
   return best_plan;
 }
+
+}  // namespace
 
 }  // namespace atlas

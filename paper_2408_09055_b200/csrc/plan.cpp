@@ -270,15 +270,20 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
   // the staging depends only on the circuit, L, G, s_max, c and the budget:
   // reuse it when atlas_plan rebuilds the plan for another ls_qubits (ls_auto)
   if (C->sp_key_valid && C->sp_key_smax == s_max && C->sp_key_c == cf &&
-      C->sp_key_budget == C->opt.stage_budget) {
+      C->sp_key_budget == C->opt.stage_budget && C->sp_key_stager == C->opt.stager &&
+      C->sp_key_regional == C->opt.regional) {
     // stage_us keeps the time of the staging that is reused
   } else {
-    C->sp = stage_circuit(n, L, G, C->info, s_max, cf, C->opt.stage_budget);
+    C->sp = C->opt.stager == 1 ? stage_greedy(n, L, G, C->info, s_max, cf)
+                               : stage_circuit(n, L, G, C->info, s_max, cf, C->opt.stage_budget,
+                                               C->opt.regional);
     C->stage_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     C->sp_key_valid = true;
     C->sp_key_smax = s_max;
     C->sp_key_c = cf;
     C->sp_key_budget = C->opt.stage_budget;
+    C->sp_key_stager = C->opt.stager;
+    C->sp_key_regional = C->opt.regional;
   }
   const int s = C->sp.s;
   C->stage_gates.assign(s, {});
@@ -529,6 +534,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           if (w.ko.algo == 1) w.kp = ordered_kernelize(w.seq, C->cm, w.ko);
           else if (w.ko.algo == 2) w.kp = greedy_kernelize(w.seq, C->cm, w.ko);
           else if (w.ko.algo == 3) w.kp = front_kernelize(w.seq, C->cm, w.ko);
+          else if (w.ko.algo == 4) w.kp = dp_only_kernelize(w.seq, C->cm, w.ko);
           else w.kp = dp_kernelize(w.seq, C->cm, w.ko);
         } catch (...) {
           errs[k] = std::current_exception();
@@ -1308,6 +1314,8 @@ std::string plan_json(const atlas_ctx *C) {
     jmask(o, C->sp.local[k]);
     o << ",\"global\":";
     jmask(o, C->sp.global[k]);
+    o << ",\"regional\":";
+    jmask(o, (C->n == 64 ? ~0ull : ((1ull << C->n) - 1)) & ~C->sp.local[k] & ~C->sp.global[k]);
     o << ",\"sigma\":[";
     for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].sigma[q];
     o << "],\"flip_begin\":[";

@@ -189,13 +189,14 @@ struct Search {
 
 struct MemoKey {
   Frontier f;
-  u64 g;
+  u64 g, b;
   int k;
-  bool operator==(const MemoKey &o) const { return g == o.g && k == o.k && f == o.f; }
+  bool operator==(const MemoKey &o) const { return g == o.g && b == o.b && k == o.k && f == o.f; }
 };
 struct MemoHash {
   size_t operator()(const MemoKey &x) const {
-    return FHash()(x.f) ^ (size_t)(x.g * 0x9E3779B97F4A7C15ull) ^ (size_t)x.k;
+    return FHash()(x.f) ^ (size_t)(x.g * 0x9E3779B97F4A7C15ull) ^ (size_t)(x.b * 0xC2B2AE3D27D4EB4Full) ^
+           (size_t)x.k;
   }
 };
 
@@ -204,10 +205,12 @@ struct MemoHash {
 // free slots), then the lowest other free qubits -- free qubits are
 // interchangeable for every later stage, so this is the cheapest and then
 // lexicographically smallest completion (R5)
-u64 fill_free(u64 c, u64 prev, u64 freeq, int G) {
+u64 fill_free(u64 c, u64 prev, u64 freeq, int G, u64 prevb = 0) {
   int need = G - popc(c);
   u64 g = c;
-  for (u64 p = prev & freeq; p && need > 0; p &= p - 1) { g |= p & (~p + 1); need--; }
+  // with regional qubits: previous globals first (no global update either)
+  for (u64 p = prevb & freeq; p && need > 0; p &= p - 1) { g |= p & (~p + 1); need--; }
+  for (u64 p = prev & freeq & ~g; p && need > 0; p &= p - 1) { g |= p & (~p + 1); need--; }
   for (u64 p = freeq & ~g; p && need > 0; p &= p - 1) { g |= p & (~p + 1); need--; }
   return need == 0 ? g : ~0ull;
 }
@@ -215,7 +218,11 @@ u64 fill_free(u64 c, u64 prev, u64 freeq, int G) {
 }  // namespace
 
 StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, int s_max,
-                        double c, long budget) {
+                        double c, long budget, int R) {
+  // G = non-local qubits (the rank bits); R of them are regional and
+  // Gg = G - R global (the paper's three tiers, Def. P:L1405-1417; R = 0 on
+  // one NVSwitch box, R > 0 emulates a two-tier interconnect, R7)
+  const int Gg = G - R;
   const int m = (int)info.size();
   for (int g = 0; g < m; g++)
     if (popc(info[g].nonins) > L)
@@ -229,9 +236,11 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
     for (auto &x : info) u |= x.nonins;
     const u64 g0 = G == 0 ? 0 : final_global(0, all & ~u, G);
     if (g0 != ~0ull) {
+      u64 b0 = 0;
+      for (u64 p = g0; p && popc(b0) < Gg; p &= p - 1) b0 |= p & (~p + 1);
       sp.s = 1;
       sp.local = {all & ~g0};
-      sp.global = {g0};
+      sp.global = {b0};
       sp.gate_stage.assign(m, 0);
       return sp;
     }
@@ -257,7 +266,20 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
       }
     }
   }
-  const double unit = 1.0 + c;
+  const double unit = 1.0 + c;  // R = 0: every swap updates a local and a global qubit
+  // the objective (Eq. P:L1491): newly local qubits + c * newly global ones
+  auto step_cost = [&](u64 g, u64 b, u64 g2, u64 b2) {
+    return R == 0 ? unit * popc(g2 & ~g) : (double)popc(g & ~g2) + c * popc(b2 & ~b);
+  };
+  // all global subsets of a non-local set (ascending); R = 0: the set itself
+  auto global_subsets = [&](u64 g2, std::vector<u64> &out) {
+    out.clear();
+    if (R == 0) {
+      out.push_back(g2);
+      return;
+    }
+    combos(g2, Gg, out);
+  };
   const Frontier empty(S.words, 0);
   // Depth-first branch and bound over the per-stage global sets, in
   // increasing bitmask order (so among plans of equal cost the first found
@@ -279,8 +301,8 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
   bool exact = true;
   int sfound = -1;
   double best_cost = 1e300;
-  std::vector<u64> best_pref;
-  auto lower_cost = [&](int s, int k, u64 g, const std::vector<int> &fw, const std::vector<int> &bw) {
+  std::vector<u64> best_pref, best_bpref;
+  auto lower_cost = [&](int s, int k, u64 g, u64 b, const std::vector<int> &fw, const std::vector<int> &bw) {
     // k = index of the stage just executed with global set g
     std::vector<u64> F(s + 1, 0);  // F[j]: qubits forced local at stage j+1 if global at j
     for (int x = 0; x < m; x++) {
@@ -291,28 +313,40 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
       for (int j = k + 1; j <= s - 2; j++)
         if (e >= j && lat <= j + 1) F[j] |= nq;
     }
-    double lb = popc(g & F[k]);
-    for (int j = k + 1; j <= s - 2; j++) lb += std::max(0, G - (n - popc(F[j])));
-    return unit * lb;
+    // forced updates: a non-local (global) qubit some remaining gate needs
+    // local at the next stage leaves the non-local (global) set
+    double lb = popc(g & F[k]), lbg = popc(b & F[k]);
+    for (int j = k + 1; j <= s - 2; j++) {
+      lb += std::max(0, G - (n - popc(F[j])));
+      lbg += std::max(0, Gg - (n - popc(F[j])));
+    }
+    return R == 0 ? unit * lb : lb + c * lbg;
   };
   for (int s = 2; s <= s_max && sfound < 0; s++) {
     const int lb0 = S.levels(empty, fwd, bwd);
     if (lb0 > s) continue;
     std::unordered_map<MemoKey, double, MemoHash> memo;
-    std::vector<u64> pref;
+    std::vector<u64> pref, bpref;
     bool stop = false;
     double root_lb = 1e300;
-    // node: stage k executed with global set g, frontier f, cost so far
-    std::function<void(int, const Frontier &, u64, double)> dfs = [&](int k, const Frontier &f, u64 g, double cost) {
+    // node: stage k executed with non-local set g (global subset b),
+    // frontier f, cost so far
+    std::function<void(int, const Frontier &, u64, u64, double)> dfs = [&](int k, const Frontier &f, u64 g,
+                                                                          u64 b, double cost) {
       if (stop) return;
       if (k == s - 2) {
         const u64 gl = final_global(g, all & ~S.remaining_nonins(f), G);
         if (gl == ~0ull) return;
-        const double tot = cost + unit * popc(gl & ~g);
+        // the last global subset: keep what can stay, then the lowest
+        u64 bl = b & gl;
+        for (u64 p = gl & ~bl; p && popc(bl) < Gg; p &= p - 1) bl |= p & (~p + 1);
+        const double tot = cost + step_cost(g, b, gl, bl);
         if (tot < best_cost) {
           best_cost = tot;
           best_pref = pref;
           best_pref.push_back(gl);
+          best_bpref = bpref;
+          best_bpref.push_back(bl);
           if (S.dbg) fprintf(stderr, "  s=%d plan cost %g evals %ld\n", s, tot, S.evals);
           if (best_cost <= root_lb) stop = true;
         }
@@ -325,7 +359,7 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
       for (int kk = kmin; kk <= std::min(G, popc(cons)); kk++) {
         combos(cons, kk, cons_sets);
         for (u64 cc : cons_sets) {
-          const u64 g2 = fill_free(cc, k < 0 ? 0 : g, freeq, G);
+          const u64 g2 = fill_free(cc, k < 0 ? 0 : g, freeq, G, k < 0 ? 0 : b);
           if (g2 == ~0ull) continue;
           // more constrained globals than needed: when every newly global
           // one could be replaced by an unused free previous global (no
@@ -338,29 +372,36 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
       std::sort(cand.begin(), cand.end());
       cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
       std::vector<int> fw, bw;
+      std::vector<u64> bsets;
       for (u64 g2 : cand) {
         if (stop) return;
         if (S.evals > S.budget) { S.over = true; stop = true; return; }
         Frontier f2 = f;
         if (S.maxexec(f2, all & ~g2) == 0) continue;
-        const double c2 = k < 0 ? 0.0 : cost + unit * popc(g2 & ~g);
         const int need = S.levels(f2, fw, bw);
         if (need > s - 1 - (k + 1)) continue;
-        if (c2 + lower_cost(s, k + 1, g2, fw, bw) >= best_cost) continue;
-        MemoKey key{f2, g2, k + 1};
-        auto it = memo.find(key);
-        if (it != memo.end() && it->second <= c2) continue;
-        memo[key] = c2;
-        pref.push_back(g2);
-        dfs(k + 1, f2, g2, c2);
-        pref.pop_back();
+        global_subsets(g2, bsets);
+        for (u64 b2 : bsets) {
+          const double c2 = k < 0 ? 0.0 : cost + step_cost(g, b, g2, b2);
+          if (c2 + lower_cost(s, k + 1, g2, b2, fw, bw) >= best_cost) continue;
+          MemoKey key{f2, g2, b2, k + 1};
+          auto it = memo.find(key);
+          if (it != memo.end() && it->second <= c2) continue;
+          memo[key] = c2;
+          pref.push_back(g2);
+          bpref.push_back(b2);
+          dfs(k + 1, f2, g2, b2, c2);
+          pref.pop_back();
+          bpref.pop_back();
+          if (stop) return;
+        }
       }
     };
     // the cost bound at the root: every boundary's unavoidable swaps
     {
       std::vector<int> fw0, bw0;
       S.levels(empty, fw0, bw0);
-      double lb = 0;
+      double lb = 0, lbg = 0;
       for (int j = 0; j <= s - 2; j++) {
         u64 Fj = 0;
         for (int x = 0; x < m; x++) {
@@ -368,10 +409,11 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
           if (e >= j && lat <= j + 1) Fj |= info[x].nonins;
         }
         lb += std::max(0, G - (n - popc(Fj)));
+        lbg += std::max(0, Gg - (n - popc(Fj)));
       }
-      root_lb = unit * lb;
+      root_lb = R == 0 ? unit * lb : lb + c * lbg;
     }
-    dfs(-1, empty, 0, 0.0);
+    dfs(-1, empty, 0, 0, 0.0);
     if (!best_pref.empty()) sfound = s;
     if (S.over) exact = false;
     if (S.dbg) fprintf(stderr, "s=%d found=%d cost %g root_lb %g evals %ld over %d\n", s, sfound, best_cost, root_lb, S.evals, (int)S.over);
@@ -386,8 +428,8 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
   sp.s = sstar;
   sp.cost = best_cost;
   sp.exact = exact;
-  sp.global = best_pref;
-  for (u64 g : sp.global) sp.local.push_back(all & ~g);
+  sp.global = best_bpref;
+  for (u64 g : best_pref) sp.local.push_back(all & ~g);
   // replay maximal execution to assign gate stages
   Frontier f = empty;
   sp.gate_stage.assign(m, -1);
@@ -399,6 +441,85 @@ StagePlan stage_circuit(int n, int L, int G, const std::vector<GateInfo> &info, 
   }
   for (int g = 0; g < m; g++)
     if (sp.gate_stage[g] < 0) fail(ATLAS_E_INFEASIBLE, "internal: staging replay incomplete");
+  sp.states_explored = S.evals;
+  return sp;
+}
+
+// The staging heuristic of SnuQS as PAPER.md describes it for its staging
+// comparison ("greedily selects the qubits with more gates
+// operating on non-local gates to form a stage and uses the number of total
+// gates as a tiebreaker").  Reading (R32): every stage takes as
+// local the L qubits with the most remaining gates that need them local
+// (the qubit is a non-insular operand), ties broken by the number of
+// remaining gates on the qubit, then by the lower index -- always including
+// the non-insular qubits of the earliest pending gate, so that every stage
+// makes progress; gates then run by maximal execution; repeat until every
+// gate has run.  The baseline of the
+// E5 experiment (tools/planner_experiments.py); option stager = 1.
+StagePlan stage_greedy(int n, int L, int G, const std::vector<GateInfo> &info, int s_max, double c) {
+  const int m = (int)info.size();
+  for (int g = 0; g < m; g++)
+    if (popc(info[g].nonins) > L)
+      fail(ATLAS_E_INFEASIBLE, "gate %d has %d non-insular qubits > L = %d", g, popc(info[g].nonins), L);
+  Search S;
+  S.n = n; S.L = L; S.G = G; S.m = m; S.words = (m + 63) / 64; S.all = full_mask(n);
+  S.info = &info; S.budget = 1;
+  S.preds.resize(m);
+  S.succs.resize(m);
+  {
+    std::vector<int> last(n, -1);
+    for (int g = 0; g < m; g++)
+      for (u64 q = info[g].qmask; q; q &= q - 1) {
+        const int b = ctz(q);
+        if (last[b] >= 0 && std::find(S.preds[g].begin(), S.preds[g].end(), last[b]) == S.preds[g].end())
+          S.preds[g].push_back(last[b]);
+        last[b] = g;
+      }
+  }
+  StagePlan sp;
+  Frontier f(S.words, 0);
+  sp.gate_stage.assign(m, -1);
+  u64 prevg = 0;
+  int ndone = 0;
+  for (int k = 0; ndone < m; k++) {
+    if (k >= s_max) fail(ATLAS_E_INFEASIBLE, "greedy staging needs more than %d stages", s_max);
+    std::vector<std::pair<std::pair<int, int>, int>> score;  // ((non-insular uses, uses), -q)
+    std::vector<int> nonl(n, 0), uses(n, 0);
+    for (int g = 0; g < m; g++) {
+      if (S.done(f, g)) continue;
+      for (u64 q = info[g].nonins; q; q &= q - 1) nonl[ctz(q)]++;
+      for (u64 q = info[g].qmask; q; q &= q - 1) uses[ctz(q)]++;
+    }
+    std::vector<int> order(n);
+    for (int q = 0; q < n; q++) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      if (nonl[a] != nonl[b]) return nonl[a] > nonl[b];
+      if (uses[a] != uses[b]) return uses[a] > uses[b];
+      return a < b;
+    });
+    // the non-insular qubits of the earliest pending gate are always local
+    // (otherwise the ranking can stall on gates blocked behind it)
+    u64 loc = 0;
+    for (int g = 0; g < m; g++)
+      if (!S.done(f, g)) {
+        loc = info[g].nonins;
+        break;
+      }
+    for (int i = 0; i < n && popc(loc) < L; i++) loc |= 1ull << order[i];
+    const Frontier before = f;
+    const int added = S.maxexec(f, loc);
+    if (added == 0) fail(ATLAS_E_INFEASIBLE, "greedy staging made no progress at stage %d", k);
+    for (int g = 0; g < m; g++)
+      if (S.done(f, g) && !S.done(before, g)) sp.gate_stage[g] = k;
+    ndone += added;
+    const u64 gl = S.all & ~loc;
+    sp.local.push_back(loc);
+    sp.global.push_back(gl);
+    if (k > 0) sp.cost += (1.0 + c) * popc(gl & ~prevg);
+    prevg = gl;
+  }
+  sp.s = (int)sp.local.size();
+  sp.exact = false;
   sp.states_explored = S.evals;
   return sp;
 }
