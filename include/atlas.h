@@ -216,6 +216,12 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
+ *   "inplace_remap"  1 = no second shard buffer: every remap runs in place
+ *                    (the pack as bit transpositions, each an in-place
+ *                    pair-swap pass; the exchange as pairwise block swaps,
+ *                    through a 256 MiB receive staging buffer with NCCL) --
+ *                    halves the HBM a rank needs (NEXT-3: n = 36 fp64 on 8
+ *                    B200s, 128 GiB shards); set before the first run [0]
  *   "shm_fuse_pack"  the local bit permutation ("pack") that precedes a
  *                    remap's exchange is folded into the store addresses of
  *                    the previous stage's last shared-memory launch, which

@@ -252,6 +252,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "ls_auto") o.ls_auto = (int)v;
     else if (k == "shm_split_dense") o.shm_split_dense = (int)v;
     else if (k == "shm_hoist_diag") o.shm_hoist_diag = (int)v;
+    else if (k == "shm_defer_diag") o.shm_defer_diag = (int)v;
     else if (k == "shm_defer_scalar") { o.shm_defer_scalar = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_swz_phase") { o.shm_swz_phase = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_tfac_min") { o.shm_tfac_min = (int)v; C->jit_ready = false; replan = false; }
@@ -259,6 +260,10 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_ctas") { need(v == 2 || v == 3, ATLAS_E_INVALID, "shm_ctas is 2 or 3"); o.shm_ctas = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_fuse_pack") o.shm_fuse_pack = (int)v;
+    else if (k == "inplace_remap") {
+      need(!C->dev_ready, ATLAS_E_ORDER, "inplace_remap must be set before the first run");
+      o.inplace_remap = (int)v;
+    }
     else if (k == "shm_grid") { need(v >= 0, ATLAS_E_INVALID, "shm_grid >= 0"); o.shm_grid = (int)v; replan = false; }
     else if (k == "shm_jit") { o.shm_jit = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "dp_budget") o.dp_budget = (long long)v;

@@ -73,11 +73,13 @@ struct Options {
   int front = 1;
   int shm_split_dense = 1;   // complex 2x2 blocks -> D1 R D2 (real R) in SHM kernels
   int shm_hoist_diag = 1;    // diagonal ops join the earliest reachable diagonal run
+  int shm_defer_diag = 1;    // diagonal ops on non-register bits wait for the next phase if one starts
   int shm_defer_scalar = 1;  // JIT: H-type blocks as adds, their uniform scale deferred
   int shm_swz_phase = 1;     // JIT: per-boundary SMEM swizzles for permuted stores
   int shm_tfac_min = 4;      // JIT: thread-only factor tables for slots with >= this many entries (0: off)
   int shm_pipe = 1;          // JIT: two thread groups per CTA on a ring of 3 tile buffers
   int shm_ctas = 2;          // JIT: resident SHM CTAs per SM for 2^12 fp64 tiles (2 or 3)
+  int inplace_remap = 0;     // remaps in place (pair swaps), no scratch shard buffer (NEXT-3)
   int shm_fuse_pack = 1;     // the remap pack fused into the previous stage's last SHM launch
   int shm_grid = 0;          // > 0: cap every SHM launch at this many CTAs (tests: many tiles per CTA at small n)
   int shm_const_pool = 0;    // JIT fp64: coefficients in a __constant__ table (c[] operands, no UMOV)
@@ -137,7 +139,9 @@ struct atlas_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  std::vector<void *> d_state, d_scratch;  // per slot
+  std::vector<void *> d_state, d_scratch;  // per slot (no scratch with option inplace_remap)
+  void *d_stage = nullptr;                 // in-place remap receive staging (multi-process)
+  size_t stage_bytes = 0;
   std::vector<int> cur;                    // 0: state holds the data, 1: scratch
   bool bound = false;
   void *d_coef = nullptr, *d_ops = nullptr, *d_phases = nullptr, *d_mats = nullptr,

@@ -14,6 +14,7 @@
 //
 // Every kernel is HBM-streaming: each launch reads and writes every amplitude
 // of the shard exactly once (2 * 2^L * sizeof(amp) algorithmic bytes).
+#include <utility>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -636,6 +637,58 @@ __global__ void __launch_bounds__(256) permute_general_kernel(const T *__restric
   }
 }
 
+// ---------------------------------------------- in-place remap (NEXT-3)
+// At HBM capacity there is no second shard buffer (n = 36 fp64 on 8 GPUs:
+// 128 GiB per shard), so the remap of P:L1312 / P:L1367-1371 runs in place
+// as a sequence of pair swaps, each a single pass with no scratch:
+//  * swap_bits_kernel: transposition of index bits a < b, i.e. the pairs
+//    (x with a=1,b=0) <-> (x with a=0,b=1) -- any local bit permutation
+//    (the "pack") is a product of at most L-1 of them;
+//  * xor_swap_kernel: x <-> x ^ F for every x whose lowest set bit of F is 0
+//    (the block relabelling that resolves the flips of incoming qubits);
+//  * swap_regions_kernel: a[i] <-> b[i] (the block exchange between two
+//    shards of a virtual world on one GPU).
+// 128-bit loads and stores; a grid-stride loop over the pairs.
+template <typename T>
+__global__ void __launch_bounds__(256) swap_bits_kernel(T *__restrict__ st, uint64_t npairs, int a, int b) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lo_a = (1ull << a) - 1, lo_b = (1ull << (b - 1)) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += stride) {
+    // deposit i around bit positions a < b (both 0), then set a
+    uint64_t x = (i & lo_a) | ((i & ~lo_a) << 1);
+    x = (x & lo_b) | ((x & ~lo_b) << 1);
+    x |= 1ull << a;
+    const uint64_t y = x ^ (1ull << a) ^ (1ull << b);
+    const T u = st[x], v = st[y];
+    st[x] = v;
+    st[y] = u;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) xor_swap_kernel(T *__restrict__ st, uint64_t npairs, uint64_t F,
+                                                       int low) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lo = (1ull << low) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += stride) {
+    const uint64_t x = (i & lo) | ((i & ~lo) << 1);  // bit `low` = 0
+    const uint64_t y = x ^ F;
+    const T u = st[x], v = st[y];
+    st[x] = v;
+    st[y] = u;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) swap_regions_kernel(T *__restrict__ a, T *__restrict__ b, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T u = a[i], v = b[i];
+    a[i] = v;
+    b[i] = u;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) scale_kernel(T *__restrict__ st, uint64_t N, double re,
                                                     double im) {
@@ -811,6 +864,36 @@ cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const in
     else
       permute_kernel<float2><<<grid, threads, 0, s>>>((const float2 *)in, (float2 *)out, N, smask, nm, a, b, c);
   }
+  return cudaGetLastError();
+}
+
+static int pair_grid(uint64_t n) {
+  const uint64_t want = (n + 255) / 256, cap = (uint64_t)num_sms() * 32;
+  return (int)(want < cap ? (want ? want : 1) : cap);
+}
+
+cudaError_t launch_swap_bits(int dtype, void *st, int L, int a, int b, cudaStream_t s) {
+  if (a == b) return cudaSuccess;
+  if (a > b) std::swap(a, b);
+  const uint64_t np = 1ull << (L - 2);
+  if (dtype == 0) swap_bits_kernel<double2><<<pair_grid(np), 256, 0, s>>>((double2 *)st, np, a, b);
+  else swap_bits_kernel<float2><<<pair_grid(np), 256, 0, s>>>((float2 *)st, np, a, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xor_swap(int dtype, void *st, int L, uint64_t F, cudaStream_t s) {
+  if (!F) return cudaSuccess;
+  const uint64_t np = 1ull << (L - 1);
+  const int low = __builtin_ctzll(F);
+  if (dtype == 0) xor_swap_kernel<double2><<<pair_grid(np), 256, 0, s>>>((double2 *)st, np, F, low);
+  else xor_swap_kernel<float2><<<pair_grid(np), 256, 0, s>>>((float2 *)st, np, F, low);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swap_regions(int dtype, void *a, void *b, uint64_t n, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  if (dtype == 0) swap_regions_kernel<double2><<<pair_grid(n), 256, 0, s>>>((double2 *)a, (double2 *)b, n);
+  else swap_regions_kernel<float2><<<pair_grid(n), 256, 0, s>>>((float2 *)a, (float2 *)b, n);
   return cudaGetLastError();
 }
 

@@ -826,13 +826,75 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
           // store map.  Ops are only reordered across ops they commute with.
           std::vector<PhaseB> phs(1);
           const int npre = (int)pre.size();
+          // a diagonal op whose tile selectors are not register bits of the
+          // current phase waits for the next dense op: if that op starts a
+          // new phase the diagonal op opens it (its selectors are then
+          // register bits there, and it joins the literal per-element factors
+          // instead of a per-thread runtime factor on every element); else it
+          // is placed in the current phase as before.  Program order is kept:
+          // it runs after every op of the current phase.
+          std::vector<int> pend;
+          PhaseB *cur = &phs.back();
+          auto fresh = [&]() {
+            phs.emplace_back();
+            cur = &phs.back();
+          };
+          auto place_diag = [&](int i) {
+            const Pre &p = pre[i];
+            int idx = i;
+            if (cur->has_perm && (p.tsel & cur->touched(K_))) {
+              Pre q;
+              if (cur->conjugate(p, tile_of_slot, K_, q)) {
+                pre.push_back(q);
+                idx = (int)pre.size() - 1;
+              } else {
+                fresh();
+              }
+            }
+            // hoist into the earliest diagonal run it can reach: it
+            // commutes with every dense op whose targets avoid its bits
+            // (all ops of a phase act on the pre-map tile index)
+            const u32 bits = pre[idx].tsel;
+            int cand = -1;
+            int at = (int)cur->items.size();
+            if (C->opt.shm_hoist_diag) {
+              for (int k2 = (int)cur->items.size() - 1; k2 >= 0; k2--) {
+                auto &it = cur->items[k2];
+                if (it.first == 1) {
+                  cand = k2;
+                  continue;
+                }
+                bool blocks = false;
+                for (int o2 : it.second)
+                  if (pre[o2].tmask & bits) blocks = true;
+                if (blocks) break;
+                at = k2;
+              }
+            }
+            const int last = (int)cur->items.size() - 1;
+            if (cand >= 0 && (cand != last || cur->diag_open)) {
+              cur->items[cand].second.push_back(idx);
+              if (cand == last) cur->diag_bits |= bits;
+              return;
+            }
+            if (!C->opt.shm_hoist_diag || at >= (int)cur->items.size()) {
+              if (!cur->diag_open) {
+                cur->items.push_back({1, {}});
+                cur->diag_open = true;
+                cur->diag_bits = 0;
+              }
+              cur->items.back().second.push_back(idx);
+              cur->diag_bits |= bits;
+            } else {
+              cur->items.insert(cur->items.begin() + at, {1, {idx}});
+            }
+          };
+          auto flush = [&]() {
+            for (int j : pend) place_diag(j);
+            pend.clear();
+          };
           for (int i = 0; i < npre; i++) {
             const Pre p = pre[i];
-            PhaseB *cur = &phs.back();
-            auto fresh = [&]() {
-              phs.emplace_back();
-              cur = &phs.back();
-            };
             bool explicit_perm = false;
             if (p.pk == PK_AFF && p.type == OP_PERM1 && C->opt.shm_explicit_perm &&
                 popc((u64)(cur->R | p.tmask)) <= RB) {
@@ -852,62 +914,27 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               }
             }
             if (p.pk == PK_AFF && !explicit_perm) {
+              flush();
               cur->aff_apply(p, tile_of_slot, K_);
               if (cur->aff_identity(K_)) cur->has_perm = false;  // e.g. CX RZ CX
               continue;
             }
             if (p.pk == PK_DIAG) {
-              int idx = i;
-              if (cur->has_perm && (p.tsel & cur->touched(K_))) {
-                Pre q;
-                if (cur->conjugate(p, tile_of_slot, K_, q)) {
-                  pre.push_back(q);
-                  idx = (int)pre.size() - 1;
-                } else {
-                  fresh();
-                }
-              }
-              // hoist into the earliest diagonal run it can reach: it
-              // commutes with every dense op whose targets avoid its bits
-              // (all ops of a phase act on the pre-map tile index)
-              const u32 bits = pre[idx].tsel;
-              int cand = -1;
-              int at = (int)cur->items.size();
-              if (C->opt.shm_hoist_diag) {
-                for (int k2 = (int)cur->items.size() - 1; k2 >= 0; k2--) {
-                  auto &it = cur->items[k2];
-                  if (it.first == 1) {
-                    cand = k2;
-                    continue;
-                  }
-                  bool blocks = false;
-                  for (int o2 : it.second)
-                    if (pre[o2].tmask & bits) blocks = true;
-                  if (blocks) break;
-                  at = k2;
-                }
-              }
-              const int last = (int)cur->items.size() - 1;
-              if (cand >= 0 && (cand != last || cur->diag_open)) {
-                cur->items[cand].second.push_back(idx);
-                if (cand == last) cur->diag_bits |= bits;
-                continue;
-              }
-              if (!C->opt.shm_hoist_diag || at >= (int)cur->items.size()) {
-                if (!cur->diag_open) {
-                  cur->items.push_back({1, {}});
-                  cur->diag_open = true;
-                  cur->diag_bits = 0;
-                }
-                cur->items.back().second.push_back(idx);
-                cur->diag_bits |= bits;
-              } else {
-                cur->items.insert(cur->items.begin() + at, {1, {idx}});
+              if (C->opt.shm_defer_diag && (p.tsel & ~cur->R)) pend.push_back(i);
+              else {
+                flush();
+                place_diag(i);
               }
               continue;
             }
-            if (cur->has_perm && ((p.tmask | p.tsel) & cur->touched(K_))) fresh();
-            if (popc((u64)(cur->R | p.tmask)) > RB) fresh();
+            const bool starts = (cur->has_perm && ((p.tmask | p.tsel) & cur->touched(K_))) ||
+                                popc((u64)(cur->R | p.tmask)) > RB;
+            if (starts) {
+              fresh();
+              flush();  // the waiting diagonal ops open the new phase
+            } else {
+              flush();
+            }
             cur->R |= p.tmask;
             if (cur->diag_open && !(p.tmask & cur->diag_bits)) {
               // commutes with the open diagonal run: execute it first
@@ -924,6 +951,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
                 cur->items.push_back({0, {i}});
             }
           }
+          flush();
           if (phs.size() > 1 && phs.back().items.empty() && !phs.back().has_perm) phs.pop_back();
           ln.sl.phase_off = (int64_t)C->phases.size();
           ln.sl.ops_off = (int64_t)C->ops.size();
@@ -1270,7 +1298,7 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
       // permuted into the other buffer, so the standalone pack pass
       // (a full read + write of the shard) disappears (P:L1312 Shard,
       // north_star (4))
-      if (C->opt.shm_fuse_pack && k + 1 < s && !SW[k + 1].pre[sl].empty() &&
+      if (C->opt.shm_fuse_pack && !C->opt.inplace_remap && k + 1 < s && !SW[k + 1].pre[sl].empty() &&
           SW[k + 1].pre[sl][0].type == L_PACK && !C->prog[sl].empty() &&
           C->prog[sl].back().type == L_SHM && C->prog[sl].back().stage == k) {
         Launch &last = C->prog[sl].back();

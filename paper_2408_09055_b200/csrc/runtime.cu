@@ -29,6 +29,9 @@ cudaError_t launch_shm(int dtype, void *st, const ShmLaunch &sl, const ShmOp *op
 cudaError_t launch_permute(int dtype, const void *in, void *out, int L, const int *newpos_host,
                            const int *newpos_dev, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void *st, int L, double re, double im, cudaStream_t s);
+cudaError_t launch_swap_bits(int dtype, void *st, int L, int a, int b, cudaStream_t s);
+cudaError_t launch_xor_swap(int dtype, void *st, int L, uint64_t F, cudaStream_t s);
+cudaError_t launch_swap_regions(int dtype, void *a, void *b, uint64_t n, cudaStream_t s);
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
 void shm_jit_prepare(atlas_ctx *C);
 cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode);
@@ -116,7 +119,7 @@ void ensure_device(atlas_ctx *C) {
     for (int s = 0; s < slots; s++) {
       if (cudaMalloc(&C->d_state[s], b) != cudaSuccess)
         fail(ATLAS_E_OOM, "cudaMalloc(%zu) state failed", b);
-      if (C->world > 1 && cudaMalloc(&C->d_scratch[s], b) != cudaSuccess)
+      if (C->world > 1 && !C->opt.inplace_remap && cudaMalloc(&C->d_scratch[s], b) != cudaSuccess)
         fail(ATLAS_E_OOM, "cudaMalloc(%zu) scratch failed", b);
     }
   }
@@ -127,6 +130,12 @@ void ensure_device(atlas_ctx *C) {
     memcpy(u.internal, C->nccl_uid, 128);
     auto init = (int (*)(void **, int, Uid, int))g_nccl.commInitRank;
     NK(init(&C->nccl_comm, C->world, u, C->rank));
+  }
+  if (C->world > 1 && C->opt.inplace_remap && C->nslots == 1 && !C->d_stage) {
+    // receive staging of the in-place exchange: one chunk
+    C->stage_bytes = std::min<size_t>(shard_bytes(C), (size_t)256 << 20);
+    if (cudaMalloc(&C->d_stage, C->stage_bytes) != cudaSuccess)
+      fail(ATLAS_E_OOM, "cudaMalloc(%zu) remap staging failed", C->stage_bytes);
   }
   C->dev_ready = true;
 }
@@ -247,6 +256,91 @@ static void do_exchange(atlas_ctx *C, int k) {
   C->cur[0] ^= 1;
 }
 
+// In-place remap (NEXT-3: no second shard buffer at HBM capacity).  The
+// pack is a product of bit transpositions (each one in-place pair-swap
+// pass); the exchange swaps, for every peer, the block it needs with the
+// block it sends -- the schedule of exchange_schedule sends block b to the
+// peer whose swapped bits are b and receives that peer's block at
+// (its swapped bits ^ incoming flips), i.e. at the SAME offset up to the
+// flip relabelling, which one xor-swap pass applies afterwards.
+static void pack_inplace(atlas_ctx *C, int s, const int *newpos) {
+  const int dt = C->dt == ATLAS_C128 ? 0 : 1;
+  const int L = C->L;
+  // realise out[newpos(i)] = in[i]: bit j of the input index ends at newpos[j]
+  std::vector<int> at(L), who(L);  // at[j]: where input bit j sits now; who[p]: which input bit sits at p
+  for (int j = 0; j < L; j++) at[j] = who[j] = j;
+  for (int j = 0; j < L; j++) {
+    const int t = newpos[j];
+    const int p = at[j];
+    if (p == t) continue;
+    CK(launch_swap_bits(dt, cur_buf(C, s), L, p, t, C->stream));
+    const int other = who[t];
+    who[t] = j;
+    at[j] = t;
+    who[p] = other;
+    at[other] = p;
+  }
+}
+
+static void exchange_inplace(atlas_ctx *C, int k) {
+  const Exchange &ex = C->exch[k];
+  const int gp = ex.gp;
+  if (gp == 0) return;
+  const int dt = C->dt == ATLAS_C128 ? 0 : 1;
+  const size_t B = amp_bytes(C);
+  const uint64_t blk = 1ull << (C->L - gp);  // amplitudes per block
+  u64 Gam = 0;
+  uint64_t f = 0;
+  for (int j = 0; j < gp; j++) {
+    Gam |= 1ull << ex.gamma[j];
+    f |= (uint64_t)ex.fI[j] << j;
+  }
+  auto bits = [&](int r) {  // swapped bits of rank r
+    int b = 0;
+    for (int j = 0; j < gp; j++) b |= ((r >> ex.gamma[j]) & 1) << j;
+    return b;
+  };
+  auto peer_of = [&](int r, int d) {  // the rank whose swapped bits are bits(r) ^ d
+    int p = r;
+    for (int j = 0; j < gp; j++)
+      if ((d >> j) & 1) p ^= 1 << ex.gamma[j];
+    return p;
+  };
+  if (C->nslots > 1) {
+    for (int r = 0; r < C->nslots; r++)
+      for (int d = 1; d < (1 << gp); d++) {
+        const int p = peer_of(r, d);
+        if (p < r) continue;
+        char *a = (char *)cur_buf(C, r) + (uint64_t)bits(p) * blk * B;
+        char *b = (char *)cur_buf(C, p) + (uint64_t)bits(r) * blk * B;
+        CK(launch_swap_regions(dt, a, b, blk, C->stream));
+      }
+    for (int r = 0; r < C->nslots; r++)
+      CK(launch_xor_swap(dt, cur_buf(C, r), C->L, f << (C->L - gp), C->stream));
+    return;
+  }
+  if (C->world == 1) return;
+  // one process per GPU: a perfect matching per step d (every rank pairs
+  // with the rank whose swapped bits differ by d), chunked through the
+  // staging buffer: send my chunk, receive the peer's into staging, then
+  // copy staging over the chunk just sent (stream order)
+  char *sh = (char *)cur_buf(C, 0);
+  const uint64_t chunk = std::max<uint64_t>(1, C->stage_bytes / B);
+  for (int d = 1; d < (1 << gp); d++) {
+    const int p = peer_of(C->rank, d);
+    char *base = sh + (uint64_t)bits(p) * blk * B;
+    for (uint64_t o = 0; o < blk; o += chunk) {
+      const uint64_t n = std::min<uint64_t>(chunk, blk - o);
+      NK(g_nccl.groupStart());
+      NK(g_nccl.send(base + o * B, n * B, kNcclUint8, p, C->nccl_comm, C->stream));
+      NK(g_nccl.recv(C->d_stage, n * B, kNcclUint8, p, C->nccl_comm, C->stream));
+      NK(g_nccl.groupEnd());
+      CK(cudaMemcpyAsync(base + o * B, C->d_stage, n * B, cudaMemcpyDeviceToDevice, C->stream));
+    }
+  }
+  CK(launch_xor_swap(dt, sh, C->L, f << (C->L - gp), C->stream));
+}
+
 void run(atlas_ctx *C) {
   if (!C->planned) fail(ATLAS_E_ORDER, "atlas_run before atlas_plan");
   ensure_device(C);
@@ -313,15 +407,20 @@ void run(atlas_ctx *C) {
         while (pc[s] < P.size() && P[pc[s]].stage == k && P[pc[s]].type == L_PACK) {
           const Launch &ln = P[pc[s]++];
           mark(L_PACK, ln.bytes);
-          CK(launch_permute(dt, cur_buf(C, s), other_buf(C, s), C->L, &C->newpos[ln.newpos_off],
-                            (const int *)C->d_newpos + ln.newpos_off, C->stream));
+          if (C->opt.inplace_remap) {
+            pack_inplace(C, s, &C->newpos[ln.newpos_off]);
+          } else {
+            CK(launch_permute(dt, cur_buf(C, s), other_buf(C, s), C->L, &C->newpos[ln.newpos_off],
+                              (const int *)C->d_newpos + ln.newpos_off, C->stream));
+            C->cur[s] ^= 1;
+          }
           mark_end();
-          C->cur[s] ^= 1;
         }
         if (pc[s] < P.size() && P[pc[s]].stage == k && P[pc[s]].type == L_EXCHANGE) pc[s]++;
       }
       mark(L_EXCHANGE, C->prog[0].empty() ? 0 : (int64_t)((double)shard_bytes(C) * (1.0 - std::ldexp(1.0, -C->exch[k].gp))) * C->nslots);
-      do_exchange(C, k);
+      if (C->opt.inplace_remap) exchange_inplace(C, k);
+      else do_exchange(C, k);
       mark_end();
     }
     for (int s = 0; s < C->nslots; s++) {
@@ -484,7 +583,7 @@ void destroy(atlas_ctx *C) {
         if (C->d_state[s]) cudaFree(C->d_state[s]);
         if (C->d_scratch[s]) cudaFree(C->d_scratch[s]);
       }
-    for (void *p : {C->d_coef, C->d_ops, C->d_phases, C->d_mats, C->d_newpos, C->d_ents, C->d_terms})
+    for (void *p : {C->d_coef, C->d_ops, C->d_phases, C->d_mats, C->d_newpos, C->d_ents, C->d_terms, C->d_stage})
       if (p) cudaFree(p);
     for (auto e : C->ev) cudaEventDestroy(e);
     if (C->own_stream) cudaStreamDestroy(C->stream);

@@ -155,3 +155,35 @@ def test_fused_pack_present():
         pj = s.plan_json()
     packed = [st for st in pj["stages"] if st["packed"]]
     assert packed and all(st["pack_fused"] for st in packed)
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+@pytest.mark.parametrize("fam", ["su2random", "qft", "random"])
+def test_inplace_remap(fam, W):
+    """NEXT-3: remaps in place (bit-transposition packs, pairwise block swaps,
+    flip relabelling; no scratch shard buffer) against O1.  The random
+    circuits put X/Y gates on global qubits, so incoming flips are exercised."""
+    c = C.random_circuit(16, 160, 60 + W, max_arity=2) if fam == "random" else C.make(fam, 18)
+    (psi,), _ = run(c, world=W, inplace_remap=1)
+    check(psi, O.simulate(c))
+
+
+def test_inplace_remap_capacity_n33_two_shards():
+    """Two 64 GiB fp64 shards of an n = 33 state on one B200 (virtual world
+    W = 2) with in-place remaps: 128 GiB total, which does not fit with a
+    scratch buffer per shard (256 GiB).  qft from |x> against the P4 closed
+    form at sampled amplitudes."""
+    n = 33
+    x = 0x15A3C1F7 & ((1 << n) - 1)
+    c = C.prepend_basis(C.qft(n), x)
+    rev = int(format(x, f"0{n}b")[::-1], 2)
+    rng = np.random.default_rng(8)
+    idx = sorted({0, (1 << n) - 1} | {int(v) for v in rng.integers(0, 1 << n, size=48)})
+    with A.Simulator(n, 0, 2, 0, virtual_world=1, inplace_remap=1) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        assert s.plan_stats()["remaps"] >= 1
+        s.run()
+        got = np.array([s.get_state(i, 1)[0] for i in idx])
+    want = np.array([np.exp(2j * np.pi * ((rev * y) % (1 << n)) / (1 << n)) for y in idx]) * 2 ** (-n / 2)
+    assert np.abs(got - want).max() <= 1e-10
