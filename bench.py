@@ -380,6 +380,16 @@ def run_atlas(args):
                 "bytes_per_launch": int(bytes_per)}
     kinds_ms = {k: round(v[0] / args.steps, 4) for k, v in by.items()}
     remap_ms = sum(t for k, t, b in launches if k == "exchange") / args.steps
+    # NVLink roofline of the inter-stage all-to-all (north_star): algorithmic
+    # bytes each rank sends per remap, (1 - 2^-g') 2^L B, over the measured
+    # peer-copy bandwidth per direction (B200_PROFILING.md: 770 GB/s)
+    nvlink = None
+    xb = sum(b for k, t, b in launches if k == "exchange")
+    if world > 1 and remap_ms > 0:
+        ach = (xb / args.steps) / (remap_ms / 1e3) / 1e9  # this rank's bytes / its remap time
+        nvlink = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 770.0, "unit": "GB/s",
+                  "frac": round(ach / 770.0, 4), "peak_source": "B200_PROFILING.md measured peer copy per direction",
+                  "bytes_per_step": int(xb / args.steps), "remap_ms_per_step": round(remap_ms, 4)}
     n_launch = sum(1 for k, t, b in launches if k in ("fused", "shm", "pack", "scale", "init"))
 
     # e2e: host buffers through the public API.  N = 1: every step uploads
@@ -410,17 +420,31 @@ def run_atlas(args):
             h2d, d2h = count * amp, count * amp
             inc = "set_state(full state from pinned host) + run + get_state(full state -> pinned host)"
         else:
-            host = torch.empty(amp, dtype=torch.uint8, pin_memory=True)
-            arr, mg = A.encode_gates(circ.gates)
+            # N > 1: the plan is preprocessing as at N = 1; every step each
+            # rank uploads its logical block [r 2^L, (r+1) 2^L) of the
+            # initial state from pinned host memory, runs, and reads its
+            # logical block of the result back (atlas_set_state /
+            # atlas_get_state fill the entries the rank owns)
+            count = 1 << (n - int(math.log2(world)))
+            h_in = torch.zeros(count * amp, dtype=torch.uint8, pin_memory=True)
+            if rank == 0:
+                h_in[:amp].view(torch.float64 if amp == 16 else torch.float32)[0] = 1.0
+            h_out = torch.empty(count * amp, dtype=torch.uint8, pin_memory=True)
+            sim.set_option("timing", 0)
+            sim.set_option("init", 0)
+            first = rank * count
+            barrier()
             t0 = time.perf_counter()
             for _ in range(reps):
-                sim.load_circuit(circ.gates)
-                sim.plan(16, 3.0)
+                sim.set_state_from(h_in.data_ptr(), first, count)
                 sim.run()
-                sim.get_state_into(host.data_ptr(), 0, 1)
+                sim.get_state_into(h_out.data_ptr(), first, count)
+            torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) / reps
-            h2d, d2h = mg * ctypes.sizeof(A.Gate), amp
-            inc = "load_circuit + plan + run + get_state(1 amplitude)"
+            sim.set_option("init", 1)
+            h2d, d2h = count * amp, count * amp
+            inc = ("per rank: set_state(its logical block from pinned host) + run + "
+                   "get_state(its logical block -> pinned host); plan = preprocessing")
         if dist is not None:
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -455,6 +479,7 @@ def run_atlas(args):
                    "remap_ms_per_step": round(remap_ms, 4),
                    "kernels_ms_per_step_total": round(step_kernel_ms, 4)},
         "roofline": roof,
+        "nvlink": nvlink,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_launch,

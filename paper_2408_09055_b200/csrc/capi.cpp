@@ -253,6 +253,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_split_dense") o.shm_split_dense = (int)v;
     else if (k == "shm_hoist_diag") o.shm_hoist_diag = (int)v;
     else if (k == "shm_defer_diag") o.shm_defer_diag = (int)v;
+    else if (k == "shm_hoist_dense") o.shm_hoist_dense = (int)v;
     else if (k == "shm_defer_scalar") { o.shm_defer_scalar = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_swz_phase") { o.shm_swz_phase = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_tfac_min") { o.shm_tfac_min = (int)v; C->jit_ready = false; replan = false; }

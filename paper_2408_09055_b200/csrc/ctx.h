@@ -73,6 +73,7 @@ struct Options {
   int front = 1;
   int shm_split_dense = 1;   // complex 2x2 blocks -> D1 R D2 (real R) in SHM kernels
   int shm_hoist_diag = 1;    // diagonal ops join the earliest reachable diagonal run
+  int shm_hoist_dense = 1;   // dense ops join the earliest dense item they commute back to
   int shm_defer_diag = 1;    // diagonal ops on non-register bits wait for the next phase if one starts
   int shm_defer_scalar = 1;  // JIT: H-type blocks as adds, their uniform scale deferred
   int shm_swz_phase = 1;     // JIT: per-boundary SMEM swizzles for permuted stores

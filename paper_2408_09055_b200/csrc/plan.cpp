@@ -936,6 +936,45 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
               flush();
             }
             cur->R |= p.tmask;
+            if (C->opt.shm_hoist_dense) {
+              // hoist: the dense op joins the earliest dense item of the phase
+              // it commutes back to (diagonal runs not acting on its targets,
+              // dense items on disjoint bits); the front packing interleaves
+              // a layer's single-qubit gates with other gates, which otherwise
+              // alternates one-gate dense items with diagonal runs
+              int at = (int)cur->items.size();
+              for (int k2 = (int)cur->items.size() - 1; k2 >= 0; k2--) {
+                const auto &it = cur->items[k2];
+                bool conf = false;
+                for (int o2 : it.second) {
+                  const Pre &q = pre[o2];
+                  if (it.first == 1 ? (q.tsel & p.tmask) != 0
+                                    : ((q.tmask & (p.tmask | p.tsel)) | (q.tsel & p.tmask)) != 0) {
+                    conf = true;
+                    break;
+                  }
+                }
+                if (conf) break;
+                at = k2;
+              }
+              int j = -1;
+              for (int k2 = at; k2 < (int)cur->items.size(); k2++)
+                if (cur->items[k2].first == 0) {
+                  j = k2;
+                  break;
+                }
+              if (j >= 0) {
+                cur->items[j].second.push_back(i);
+                continue;
+              }
+              if (at < (int)cur->items.size()) {
+                cur->items.insert(cur->items.begin() + at, {0, {i}});
+                continue;
+              }
+              cur->diag_open = false;
+              cur->items.push_back({0, {i}});
+              continue;
+            }
             if (cur->diag_open && !(p.tmask & cur->diag_bits)) {
               // commutes with the open diagonal run: execute it first
               const size_t n_it = cur->items.size();

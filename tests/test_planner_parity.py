@@ -229,3 +229,40 @@ def test_front_packing_cx_block_windows():
     pa = product_plan(c, 1, kernelizer=3, kinds=2)
     assert pa["ls_qubits"] in (4, 5)
     assert len(pa["stages"][0]["kernels"]) <= 3
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_exchange_is_pairwise_swap_up_to_flip_relabel(seed, W):
+    """The property the in-place remap (option inplace_remap, NEXT-3) relies
+    on: in every remap, each rank sends to peer p the block at offset o and
+    receives p's block at o XOR (incoming flips, as a block index) -- the
+    same relabelling for every peer and for the block that stays local -- and
+    p does the mirror image.  So a pairwise in-place block swap followed by
+    one xor relabel pass reproduces the out-of-place exchange exactly."""
+    n = 10
+    c = C.random_circuit(n, 60, 500 + seed, kinds=("H", "X", "Y", "CX", "CZ", "RZ", "U3", "SWAP"),
+                         max_arity=2)
+    scheds = []
+    for r in range(W):
+        with A.Simulator(n, 0, W, r) as s:
+            s.load_circuit(c.gates)
+            s.plan()
+            S = s.plan_json()["staging"]["s"]
+            scheds.append({k: s.remap_schedule(k) for k in range(1, S)})
+    for k in scheds[0]:
+        for r in range(W):
+            xs = scheds[r][k]
+            if not xs:
+                continue
+            sends = {x[1]: x[2] for x in xs if x[0] == "send"}
+            recvs = {x[1]: x[3] for x in xs if x[0] == "recv"}
+            local = [x for x in xs if x[0] == "local"]
+            assert len(local) == 1 and set(sends) == set(recvs)
+            rel = local[0][2] ^ local[0][3]  # the flip relabel of this remap (bytes)
+            for p, so in sends.items():
+                assert recvs[p] ^ so == rel
+                # the peer's pair of transfers with us has the same shape
+                psend = {x[1]: x[2] for x in scheds[p][k] if x[0] == "send"}
+                prec = {x[1]: x[3] for x in scheds[p][k] if x[0] == "recv"}
+                assert prec[r] ^ psend[r] == rel
