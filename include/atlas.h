@@ -216,6 +216,14 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
+ *   "offload"        R > 0: host-DRAM tier (NEXT-4; the paper's regional
+ *                    qubits in DRAM, Def. P:L1405-1417): the
+ *                    state lives in two pinned host buffers of 2^n
+ *                    amplitudes; planned as 2^R shards of 2^(n-R) whose
+ *                    non-local qubits are regional; every stage streams each
+ *                    shard through the GPU (H2D gathers perform the remap's
+ *                    exchange, kernels, pack, D2H).  Needs world = 1; set
+ *                    before the first run [0]
  *   "inplace_remap"  1 = no second shard buffer: every remap runs in place
  *                    (the pack as bit transpositions, each an in-place
  *                    pair-swap pass; the exchange as pairwise block swaps,
@@ -304,7 +312,8 @@ atlas_status atlas_get_jit_source(atlas_ctx *ctx, int slot, int index, char *buf
 
 /* Per-launch records of the last atlas_run (needs option "timing" = 1):
  * ms[i] device time, kind[i] (0 init, 1 fused, 2 shm, 3 pack, 4 exchange,
- * 5 scale), bytes[i] algorithmic HBM bytes of that launch (read + write of
+ * 5 scale, 6 host-to-device and 7 device-to-host shard copies of the
+ * offload tier), bytes[i] algorithmic HBM bytes of that launch (read + write of
  * the amplitudes it touches).  *count receives the number of records. */
 atlas_status atlas_get_launches(atlas_ctx *ctx, float *ms, int32_t *kind,
                                 int64_t *bytes, int cap, int *count);

@@ -25,7 +25,7 @@ KIND = {k: i for i, k in enumerate(
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_INFEASIBLE", 4: "E_BUDGET",
           5: "E_OOM", 6: "E_CUDA", 7: "E_NCCL", 8: "E_ORDER"}
 
-LAUNCH_KIND = {0: "init", 1: "fused", 2: "shm", 3: "pack", 4: "exchange", 5: "scale"}
+LAUNCH_KIND = {0: "init", 1: "fused", 2: "shm", 3: "pack", 4: "exchange", 5: "scale", 6: "h2d", 7: "d2h"}
 
 # exported symbols (include/atlas.h); the CPU test checks each is present
 SYMBOLS = [

@@ -261,7 +261,20 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_ctas") { need(v == 2 || v == 3, ATLAS_E_INVALID, "shm_ctas is 2 or 3"); o.shm_ctas = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_fuse_pack") o.shm_fuse_pack = (int)v;
-    else if (k == "inplace_remap") {
+    else if (k == "offload") {
+      // R regional qubits held in host DRAM: planned like a virtual world of
+      // 2^R shards whose non-local qubits are all regional (the staging
+      // objective counts newly local qubits, Eq. P:L1491 with G = 0)
+      need(!C->dev_ready, ATLAS_E_ORDER, "offload must be set before the first run");
+      need(C->world == 1 || C->offload > 0, ATLAS_E_UNSUPPORTED, "offload needs world == 1");
+      need(v >= 0 && v < C->n && v <= 10, ATLAS_E_INVALID, "offload in [0, min(n-1, 10)]");
+      C->offload = (int)v;
+      C->world = 1 << v;
+      C->G = (int)v;
+      C->L = C->n - (int)v;
+      o.virtual_world = v > 0 ? 1 : 0;
+      o.regional = (int)v;
+    } else if (k == "inplace_remap") {
       need(!C->dev_ready, ATLAS_E_ORDER, "inplace_remap must be set before the first run");
       o.inplace_remap = (int)v;
     }

@@ -10,7 +10,8 @@
 
 namespace atlas {
 
-enum LaunchType { L_INIT = 0, L_FUSED = 1, L_SHM = 2, L_PACK = 3, L_EXCHANGE = 4, L_SCALE = 5 };
+enum LaunchType { L_INIT = 0, L_FUSED = 1, L_SHM = 2, L_PACK = 3, L_EXCHANGE = 4, L_SCALE = 5,
+                  L_H2D = 6, L_D2H = 7 };
 
 struct Launch {
   int type = 0;
@@ -142,6 +143,14 @@ struct atlas_ctx {
   bool own_stream = false;
   std::vector<void *> d_state, d_scratch;  // per slot (no scratch with option inplace_remap)
   void *d_stage = nullptr;                 // in-place remap receive staging (multi-process)
+  // host-DRAM offload tier (option offload = R, NEXT-4): the 2^R shards
+  // ("regional" chunks, Def. P:L1405-1417) live in two pinned host buffers
+  // (ping-pong across stages); each stage streams every shard through the
+  // two device work buffers
+  int offload = 0;
+  void *h_buf[2] = {nullptr, nullptr};
+  int h_cur = 0;
+  void *d_work[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;
   std::vector<int> cur;                    // 0: state holds the data, 1: scratch
   bool bound = false;

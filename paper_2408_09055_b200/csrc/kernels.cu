@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(256) permute_general_kernel(const T *__restric
 template <typename T>
 __global__ void __launch_bounds__(256) swap_bits_kernel(T *__restrict__ st, uint64_t npairs, int a, int b) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t lo_a = (1ull << a) - 1, lo_b = (1ull << (b - 1)) - 1;
+  const uint64_t lo_a = (1ull << a) - 1, lo_b = (1ull << b) - 1;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += stride) {
     // deposit i around bit positions a < b (both 0), then set a
     uint64_t x = (i & lo_a) | ((i & ~lo_a) << 1);

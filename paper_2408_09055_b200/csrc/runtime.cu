@@ -112,6 +112,21 @@ void ensure_device(atlas_ctx *C) {
   }
   const int slots = C->nslots;
   C->cur.assign(slots, 0);
+  if (C->offload) {
+    // two pinned host copies of the whole state (stage ping-pong) and two
+    // device work shards (the second receives a fused pack's output)
+    const size_t hb = amp_bytes(C) << C->n;
+    for (int i = 0; i < 2; i++) {
+      if (cudaHostAlloc(&C->h_buf[i], hb, cudaHostAllocDefault) != cudaSuccess)
+        fail(ATLAS_E_OOM, "cudaHostAlloc(%zu) offload host buffer failed", hb);
+      if (cudaMalloc(&C->d_work[i], shard_bytes(C)) != cudaSuccess)
+        fail(ATLAS_E_OOM, "cudaMalloc(%zu) offload work shard failed", shard_bytes(C));
+    }
+    C->d_state.assign(slots, nullptr);
+    C->d_scratch.assign(slots, nullptr);
+    C->dev_ready = true;
+    return;
+  }
   if (!C->bound) {
     C->d_state.assign(slots, nullptr);
     C->d_scratch.assign(slots, nullptr);
@@ -341,6 +356,141 @@ static void exchange_inplace(atlas_ctx *C, int k) {
   CK(launch_xor_swap(dt, sh, C->L, f << (C->L - gp), C->stream));
 }
 
+// Host-DRAM offload tier (NEXT-4; the paper's regional qubits in DRAM,
+// Def. P:L1405-1417).  Stage k streams every shard s through
+// the GPU: its blocks are gathered from host buffer h_cur by H2D copies
+// following stage k's exchange schedule (the all-to-all becomes a choice of
+// source addresses), the stage's kernels run, the next remap's pack runs
+// (fused into the last shared-memory launch, or standalone), and the shard
+// goes back by D2H into the other host buffer.
+static void run_offload(atlas_ctx *C) {
+  const int dt = C->dt == ATLAS_C128 ? 0 : 1;
+  const size_t SB = shard_bytes(C);
+  const bool timing = C->opt.timing != 0;
+  std::vector<std::pair<int, int64_t>> rec;
+  size_t nev = 0;
+  auto ev_at = [&](size_t i) {
+    while (C->ev.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      C->ev.push_back(e);
+    }
+    return C->ev[i];
+  };
+  auto mark = [&](int kind, int64_t bytes) {
+    if (!timing) return;
+    CK(cudaEventRecord(ev_at(nev++), C->stream));
+    rec.push_back({kind, bytes});
+  };
+  auto mark_end = [&]() {
+    if (timing) CK(cudaEventRecord(ev_at(nev++), C->stream));
+  };
+  const bool from_host = !C->opt.init && C->state_set;
+  if (!C->opt.init && !C->state_set) fail(ATLAS_E_ORDER, "option init=0 but no atlas_set_state");
+  C->state_set = false;
+  C->h_cur = 0;
+  const double2 *mats = (const double2 *)C->d_mats;
+  const int S = C->sp.s;
+  std::vector<size_t> pc(C->nslots, 0);
+  for (int k = 0; k < S; k++) {
+    char *hsrc = (char *)C->h_buf[C->h_cur];
+    char *hdst = (char *)C->h_buf[C->h_cur ^ 1];
+    for (int s = 0; s < C->nslots; s++) {
+      auto &P = C->prog[s];
+      int w = 0;  // device work shard holding the data
+      int zm = 0;
+      if (k == 0 && !from_host) {
+        if (C->opt.init_fuse && !P.empty() && P[0].type == L_SHM && shm_jit_zero_ok(P[0].jit)) {
+          zm = s == 0 ? 2 : 1;
+        } else {
+          mark(L_INIT, (int64_t)SB);
+          CK(launch_init(dt, C->d_work[0], C->L, s == 0, C->stream));
+          mark_end();
+        }
+      } else if (k > 0 && C->exch[k].gp > 0) {
+        mark(L_H2D, (int64_t)SB);
+        for (const Xfer &x : exchange_schedule(C, k, s)) {
+          if (x.kind == XFER_SEND) continue;
+          uint64_t so = x.src_off;
+          const int from = x.kind == XFER_LOCAL ? s : x.peer;
+          if (x.kind == XFER_RECV)
+            for (const Xfer &y : exchange_schedule(C, k, from))
+              if (y.kind == XFER_SEND && y.peer == s) so = y.src_off;
+          CK(cudaMemcpyAsync((char *)C->d_work[0] + x.dst_off, hsrc + (size_t)from * SB + so, x.bytes,
+                             cudaMemcpyHostToDevice, C->stream));
+        }
+        mark_end();
+      } else {
+        mark(L_H2D, (int64_t)SB);
+        CK(cudaMemcpyAsync(C->d_work[0], hsrc + (size_t)s * SB, SB, cudaMemcpyHostToDevice, C->stream));
+        mark_end();
+      }
+      // the stage's launches (remap pack / exchange records of stage k were
+      // consumed above or at the end of stage k-1)
+      while (pc[s] < P.size() && P[pc[s]].stage == k && (P[pc[s]].type == L_PACK || P[pc[s]].type == L_EXCHANGE))
+        pc[s]++;
+      bool first = true;
+      while (pc[s] < P.size() && P[pc[s]].stage == k) {
+        const Launch &ln = P[pc[s]++];
+        void *st = C->d_work[w];
+        const int z = first ? zm : 0;
+        first = false;
+        mark(ln.type, z ? ln.bytes / 2 : ln.bytes);
+        switch (ln.type) {
+          case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
+          case L_SHM: {
+            ShmLaunch sl = ln.sl;
+            sl.grid_cap = C->opt.shm_grid;
+            const bool operm = sl.out_perm_off >= 0;
+            void *dst = operm ? C->d_work[w ^ 1] : st;
+            if (ln.jit) {
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z));
+            } else {
+              CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
+                            (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
+                            (const PermTerm *)C->d_terms, C->stream));
+              if (operm)
+                CK(launch_permute(dt, st, dst, C->L, &C->newpos[sl.out_perm_off],
+                                  (const int *)C->d_newpos + sl.out_perm_off, C->stream));
+            }
+            if (operm) w ^= 1;
+            break;
+          }
+          case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;
+          default: fail(ATLAS_E_INVALID, "internal: unexpected launch type %d", ln.type);
+        }
+        mark_end();
+      }
+      if (zm && first) fail(ATLAS_E_INVALID, "internal: zero-mode slot without a launch");
+      // a standalone pack of the next remap runs while the shard is here
+      if (k + 1 < S)
+        for (size_t q = pc[s]; q < P.size() && P[q].stage == k + 1 && P[q].type == L_PACK; q++) {
+          mark(L_PACK, P[q].bytes);
+          CK(launch_permute(dt, C->d_work[w], C->d_work[w ^ 1], C->L, &C->newpos[P[q].newpos_off],
+                            (const int *)C->d_newpos + P[q].newpos_off, C->stream));
+          mark_end();
+          w ^= 1;
+        }
+      mark(L_D2H, (int64_t)SB);
+      CK(cudaMemcpyAsync(hdst + (size_t)s * SB, C->d_work[w], SB, cudaMemcpyDeviceToHost, C->stream));
+      mark_end();
+    }
+    C->h_cur ^= 1;
+  }
+  CK(cudaStreamSynchronize(C->stream));
+  C->launch_ms.clear();
+  C->launch_kind.clear();
+  C->launch_bytes.clear();
+  if (timing)
+    for (size_t i = 0; i < rec.size(); i++) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, C->ev[2 * i], C->ev[2 * i + 1]));
+      C->launch_ms.push_back(ms);
+      C->launch_kind.push_back(rec[i].first);
+      C->launch_bytes.push_back(rec[i].second);
+    }
+}
+
 void run(atlas_ctx *C) {
   if (!C->planned) fail(ATLAS_E_ORDER, "atlas_run before atlas_plan");
   ensure_device(C);
@@ -352,6 +502,10 @@ void run(atlas_ctx *C) {
     if (C->opt.shm_jit) shm_jit_prepare(C);
     C->jit_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     C->jit_ready = true;
+  }
+  if (C->offload) {
+    run_offload(C);
+    return;
   }
   const int dt = C->dt == ATLAS_C128 ? 0 : 1;
   const bool timing = C->opt.timing != 0;
@@ -492,6 +646,13 @@ static bool identity_layout(const atlas_ctx *C, int stage, bool end) {
   return true;
 }
 
+// The data of shard s: a device pointer, or (offload tier) a host pointer
+// into the pinned buffer that holds the current stage layout.
+static char *shard_data(atlas_ctx *C, int s, bool stage0) {
+  if (C->offload) return (char *)C->h_buf[stage0 ? 0 : C->h_cur] + (size_t)s * shard_bytes(C);
+  return (char *)(stage0 ? C->d_state[s] : cur_buf(C, s));
+}
+
 void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
   if (!C->planned || !C->dev_ready) fail(ATLAS_E_ORDER, "atlas_get_state before atlas_run");
   if (count == 0) return;
@@ -499,6 +660,7 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
   const size_t B = amp_bytes(C);
   const int last = C->sp.s - 1;
   CK(cudaSetDevice(C->device));
+  const cudaMemcpyKind kind = C->offload ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost;
   if (identity_layout(C, last, true)) {
     // physical == logical: contiguous copies per shard
     uint64_t x = first, end = first + count;
@@ -508,18 +670,39 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
       uint64_t len = std::min<uint64_t>(end - x, (1ull << C->L) - off);
       int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
       if (s >= 0)
-        CK(cudaMemcpyAsync((char *)host + (x - first) * B, (const char *)cur_buf(C, s) + off * B,
-                           len * B, cudaMemcpyDeviceToHost, C->stream));
+        CK(cudaMemcpyAsync((char *)host + (x - first) * B, shard_data(C, s, false) + off * B, len * B, kind,
+                           C->stream));
       x += len;
     }
     CK(cudaStreamSynchronize(C->stream));
     return;
   }
-  // general layout: bring the shard(s) to the host and gather
-  std::vector<std::vector<char>> sh(C->nslots);
+  // general layout, few amplitudes (sampled checks at capacity): one small
+  // copy per amplitude instead of moving whole shards
+  if (!C->offload && count <= 4096 && count * 64 < (1ull << C->L)) {
+    for (uint64_t i = 0; i < count; i++) {
+      int r;
+      uint64_t off;
+      locate(C, last, first + i, &r, &off);
+      int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
+      if (s < 0) continue;
+      CK(cudaMemcpyAsync((char *)host + i * B, (const char *)cur_buf(C, s) + off * B, B,
+                         cudaMemcpyDeviceToHost, C->stream));
+    }
+    CK(cudaStreamSynchronize(C->stream));
+    return;
+  }
+  // general layout: the shard(s) on the host, then gather
+  std::vector<std::vector<char>> sh(C->offload ? 0 : C->nslots);
+  std::vector<const char *> src(C->nslots);
   for (int s = 0; s < C->nslots; s++) {
+    if (C->offload) {
+      src[s] = shard_data(C, s, false);
+      continue;
+    }
     sh[s].resize(shard_bytes(C));
     CK(cudaMemcpy(sh[s].data(), cur_buf(C, s), shard_bytes(C), cudaMemcpyDeviceToHost));
+    src[s] = sh[s].data();
   }
   for (uint64_t i = 0; i < count; i++) {
     int r;
@@ -527,7 +710,7 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
     locate(C, last, first + i, &r, &off);
     int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
     if (s < 0) continue;
-    memcpy((char *)host + i * B, sh[s].data() + off * B, B);
+    memcpy((char *)host + i * B, src[s] + off * B, B);
   }
 }
 
@@ -538,6 +721,7 @@ void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
   CK(cudaSetDevice(C->device));
   const size_t B = amp_bytes(C);
   for (int s = 0; s < C->nslots; s++) C->cur[s] = 0;
+  const cudaMemcpyKind kind = C->offload ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice;
   if (identity_layout(C, 0, false)) {
     // logical == physical at stage 0: contiguous copies into each shard
     uint64_t x = first, end = first + count;
@@ -547,8 +731,8 @@ void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
       uint64_t len = std::min<uint64_t>(end - x, (1ull << C->L) - off);
       int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
       if (s >= 0)
-        CK(cudaMemcpyAsync((char *)C->d_state[s] + off * B, (const char *)host + (x - first) * B,
-                           len * B, cudaMemcpyHostToDevice, C->stream));
+        CK(cudaMemcpyAsync(shard_data(C, s, true) + off * B, (const char *)host + (x - first) * B, len * B,
+                           kind, C->stream));
       x += len;
     }
     CK(cudaStreamSynchronize(C->stream));
@@ -556,10 +740,16 @@ void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
     return;
   }
   // general stage-0 layout: scatter on the host
-  std::vector<std::vector<char>> sh(C->nslots);
+  std::vector<std::vector<char>> sh(C->offload ? 0 : C->nslots);
+  std::vector<char *> dst(C->nslots);
   for (int s = 0; s < C->nslots; s++) {
+    if (C->offload) {
+      dst[s] = shard_data(C, s, true);
+      continue;
+    }
     sh[s].resize(shard_bytes(C));
     CK(cudaMemcpy(sh[s].data(), C->d_state[s], shard_bytes(C), cudaMemcpyDeviceToHost));
+    dst[s] = sh[s].data();
   }
   for (uint64_t i = 0; i < count; i++) {
     int r;
@@ -567,10 +757,11 @@ void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
     locate(C, 0, first + i, &r, &off);
     int s = C->nslots > 1 ? r : (r == C->rank ? 0 : -1);
     if (s < 0) continue;
-    memcpy(sh[s].data() + off * B, (const char *)host + i * B, B);
+    memcpy(dst[s] + off * B, (const char *)host + i * B, B);
   }
-  for (int s = 0; s < C->nslots; s++)
-    CK(cudaMemcpy(C->d_state[s], sh[s].data(), shard_bytes(C), cudaMemcpyHostToDevice));
+  if (!C->offload)
+    for (int s = 0; s < C->nslots; s++)
+      CK(cudaMemcpy(C->d_state[s], sh[s].data(), shard_bytes(C), cudaMemcpyHostToDevice));
   C->state_set = true;
 }
 
@@ -578,6 +769,10 @@ void destroy(atlas_ctx *C) {
   if (C->dev_ready) {
     cudaSetDevice(C->device);
     cudaStreamSynchronize(C->stream);
+    for (int i = 0; i < 2; i++) {
+      if (C->h_buf[i]) cudaFreeHost(C->h_buf[i]);
+      if (C->d_work[i]) cudaFree(C->d_work[i]);
+    }
     if (!C->bound)
       for (size_t s = 0; s < C->d_state.size(); s++) {
         if (C->d_state[s]) cudaFree(C->d_state[s]);

@@ -187,3 +187,31 @@ def test_inplace_remap_capacity_n33_two_shards():
         got = np.array([s.get_state(i, 1)[0] for i in idx])
     want = np.array([np.exp(2j * np.pi * ((rev * y) % (1 << n)) / (1 << n)) for y in idx]) * 2 ** (-n / 2)
     assert np.abs(got - want).max() <= 1e-10
+
+
+@pytest.mark.parametrize("R", [1, 2, 4])
+@pytest.mark.parametrize("fam", ["su2random", "qft", "ising", "random"])
+def test_offload_tier(fam, R):
+    """NEXT-4: the state in host DRAM (2^R regional chunks streamed through
+    the GPU stage by stage) against O1, element by element."""
+    c = C.random_circuit(16, 160, 80 + R, max_arity=2) if fam == "random" else C.make(fam, 18)
+    (psi,), st = run(c, offload=R)
+    assert st["G"] == R
+    check(psi, O.simulate(c))
+
+
+def test_offload_tier_from_input_state():
+    """atlas_set_state into the host tier (arbitrary input)."""
+    n = 15
+    c = C.random_circuit(n, 120, 91, max_arity=3)
+    rng = np.random.default_rng(4)
+    psi0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    with A.Simulator(n, 0, 1, 0, offload=3) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.set_option("init", 0)
+        s.set_state(psi0)
+        s.run()
+        psi = s.get_state()
+    check(psi, O.simulate(c, init=psi0))

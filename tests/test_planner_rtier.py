@@ -122,3 +122,26 @@ def test_regional_c_changes_only_the_objective_on_benchmarks():
                 for k in range(1, pj["staging"]["s"]))
         assert pj["staging"]["cost"] == pytest.approx(S + cf * T)
     assert all(p == plans[0] for p in plans)
+
+
+def _kcost(c, **opt):
+    with A.Simulator(c.n, 0, 1, 0, **opt) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        return s.plan_stats()["kernel_cost"]
+
+
+@pytest.mark.parametrize("fam", ["qft", "ising", "qsvm", "wstate", "random"])
+def test_kernelize_dp_unpruned_not_worse_than_ordered(fam):
+    """Thm. dp-optimal: without pruning (T beyond any position's
+    state count) the Kernelize DP alone is never worse than
+    OrderedKernelize; the default Kernelize (cheapest valid of DP, Ordered and
+    the front packing, R29) is never worse than either (E7's invariants)."""
+    n = 12
+    c = C.random_circuit(n, 40, 21, max_arity=2) if fam == "random" else C.make(fam, n)
+    dp = _kcost(c, kernelizer=4, prune_T=0, ls_qubits=4)
+    ordered = _kcost(c, kernelizer=1, ls_qubits=4)
+    front = _kcost(c, kernelizer=3, ls_qubits=4)
+    default = _kcost(c, kernelizer=0, ls_qubits=4)
+    assert dp <= ordered
+    assert default <= min(ordered, front)
