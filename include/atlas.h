@@ -216,6 +216,15 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
+ *   "shm_addr_split" plan-specialised kernels address a phase's shared-memory
+ *                    elements as (x ^ low) + high: one pointer per distinct
+ *                    low (bank-bit) part, immediate offsets for the rest [1]
+ *   "shm_lit_smem"   plan-specialised fp64 kernels read the per-element
+ *                    complex factors of their diagonal runs from a table in
+ *                    shared memory (one broadcast LDS.128 per element instead
+ *                    of four UMOVs materialising two literals); measured
+ *                    slower (the kernels are shared-memory/MIO bound, not
+ *                    issue bound), so off by default [0]
  *   "offload"        R > 0: host-DRAM tier (NEXT-4; the paper's regional
  *                    qubits in DRAM, Def. P:L1405-1417): the
  *                    state lives in two pinned host buffers of 2^n

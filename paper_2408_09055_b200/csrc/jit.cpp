@@ -107,6 +107,29 @@ struct LitPool {
 };
 thread_local LitPool *g_pool = nullptr;
 
+// fp64 complex factors of diagonal-run elements, read from a shared-memory
+// table (option shm_lit_smem): a uniform-address LDS.128 per element replaces
+// the four UMOVs that materialise the two literals in uniform registers
+// (UMOV was 24% of the issued instructions of su2random's heaviest kernel).
+// ptxas cannot hoist the loads out of the tile loop (the loop's shared stores
+// may alias the table), so no register is held across tiles.
+struct LitTab {
+  std::vector<std::pair<double, double>> vals;
+  std::map<std::pair<uint64_t, uint64_t>, int> index;
+  int intern(double re, double im) {
+    uint64_t a, b;
+    memcpy(&a, &re, 8);
+    memcpy(&b, &im, 8);
+    auto it = index.find({a, b});
+    if (it != index.end()) return it->second;
+    const int k = (int)vals.size();
+    vals.push_back({re, im});
+    index[{a, b}] = k;
+    return k;
+  }
+};
+thread_local LitTab *g_ltab = nullptr;
+
 std::string lit(double d, bool f32) {
   char b[64];
   if (f32) {
@@ -178,6 +201,12 @@ void emit_cmul_lit(std::ostringstream &o, int e, double re, double im, bool f32,
       << ";\n";
     return;
   }
+  if (g_ltab && !f32 && re != 0.0) {
+    const int k = g_ltab->intern(re, im);
+    o << ind << "{ const T f = lt[" << k << "]; const T a = v[" << e << "]; v[" << e
+      << "].x = f.x * a.x - f.y * a.y; v[" << e << "].y = f.x * a.y + f.y * a.x; }\n";
+    return;
+  }
   o << ind << "{ const T a = v[" << e << "]; v[" << e << "].x = " << lit(re, f32) << " * a.x - "
     << lit(im, f32) << " * a.y; v[" << e << "].y = " << lit(re, f32) << " * a.y + " << lit(im, f32)
     << " * a.x; }\n";
@@ -188,21 +217,79 @@ const int kDiagSel[11] = {0, 1, 2, 4, 8, 3, 5, 9, 6, 10, 12};
 }  // namespace
 
 int shm_nbuf_effective(int dtype, const ShmLaunch &sl);
+size_t shm_jit_smem(const std::string &src);
 
 // The straight-line source of one shared-memory launch (same skeleton as
 // kernels.cu shm_kernel: ring of tile buffers filled with cp.async, register
 // phases, permuted stores, optional direct HBM store of the last phase).
 static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, const std::string &name);
 
+// The shared-memory literal table (shm_lit_smem) goes after every other
+// shared buffer of the launch; its entries are known only once the body is
+// generated, so the table, its fill loop and the size are patched in here.
+// A launch whose table does not fit beside its resident CTAs falls back to
+// literals.
+static std::string patch_lit_table(const std::string &body, const LitTab &tab) {
+  auto drop = [&](std::string s) {
+    for (const char *ph : {"//@LT_DECL@\n", "//@LT_FILL@\n"}) {
+      const size_t at = s.find(ph);
+      if (at != std::string::npos) s.erase(at, strlen(ph));
+    }
+    return s;
+  };
+  if (tab.vals.empty()) return drop(body);
+  const size_t smem = shm_jit_smem(body);
+  const size_t lt_off = (smem + 15) & ~(size_t)15;
+  const size_t nsmem = lt_off + 16 * tab.vals.size();
+  int bt = 0, minb = 1;
+  {
+    const char *p = strstr(body.c_str(), "__launch_bounds__(");
+    if (p) sscanf(p, "__launch_bounds__(%d, %d)", &bt, &minb);
+  }
+  const size_t cap = minb >= 2 ? 233472 / minb - 1024 : 232448;
+  if (nsmem > cap) return std::string();
+  std::string s = body;
+  auto rep = [&](const std::string &from, const std::string &to) {
+    const size_t at = s.find(from);
+    if (at == std::string::npos) fail(ATLAS_E_CUDA, "shm_jit: literal table placeholder missing");
+    s.replace(at, from.size(), to);
+  };
+  std::ostringstream t;
+  t << "#define LT_OFF " << lt_off << "\n__constant__ double2 LTC[" << tab.vals.size() << "] = {";
+  char b[96];
+  for (size_t i = 0; i < tab.vals.size(); i++) {
+    snprintf(b, sizeof b, "%s{%a, %a}", i ? ", " : "", tab.vals[i].first, tab.vals[i].second);
+    t << b;
+  }
+  t << "};\n#define SMEM_BYTES " << nsmem << "\n";
+  rep("#define SMEM_BYTES " + std::to_string(smem) + "\n", t.str());
+  rep("//@LT_DECL@\n", "  T *lt = reinterpret_cast<T *>(smraw + LT_OFF);\n");
+  rep("//@LT_FILL@\n", "  for (int i = threadIdx.x; i < " + std::to_string(tab.vals.size()) +
+                           "; i += BLOCK_THREADS) lt[i] = LTC[i];\n");
+  return s;
+}
+
 std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::string &name) {
   LitPool pool;
   const bool use_pool = C->dt == ATLAS_C128 && C->opt.shm_const_pool;
   g_pool = use_pool ? &pool : nullptr;
+  LitTab tab;
+  const bool use_tab = C->dt == ATLAS_C128 && C->opt.shm_lit_smem && !use_pool;
   std::string body;
   try {
+    g_ltab = use_tab ? &tab : nullptr;
     body = shm_jit_source_body(C, sl, name);
+    g_ltab = nullptr;
+    std::string patched = patch_lit_table(body, tab);
+    if (patched.empty()) {  // the table does not fit: literals
+      pool = LitPool();
+      body = patch_lit_table(shm_jit_source_body(C, sl, name), LitTab());
+    } else {
+      body = patched;
+    }
   } catch (...) {
     g_pool = nullptr;
+    g_ltab = nullptr;
     throw;
   }
   g_pool = nullptr;
@@ -563,6 +650,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     << "(T *__restrict__ st, T *dst, int zmode) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
+  o << "//@LT_DECL@\n";
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
   o << "  u16 *stab = reinterpret_cast<u16 *>(smraw + " << off_stab << ");\n";
   o << "  u64 *btab = reinterpret_cast<u64 *>(smraw + " << off_btab << ");\n";
@@ -653,6 +741,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   for (int t = 0; t < K - RB; t++) o << " if ((tid >> " << t << ") & 1) sw_out ^= " << Sx(SO, 1u << t) << ";";
   o << "\n";
   o << "  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);\n";
+  o << "//@LT_FILL@\n";
   o << "  __syncthreads();\n";
   o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255]";
   for (int c = 1; c < nbt; c++) o << " | btab[" << 256 * c << " + ((tile >> " << 8 * c << ") & 255)]";
@@ -686,6 +775,33 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "  auto issue = [&](int bsel, int msel, u64 base) { if (!zmode) issue_load(bsel, msel, base); else asm volatile("
          "\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mbar0 + 8 * msel) : \"memory\"); };\n";
   const std::string GS = pipe ? "gsync(grp);" : "__syncthreads();";
+  // tb[x ^ a] for one thread part x and the element constants a of a phase:
+  // when x's set bits above the bank bits (W) never meet a's (x and a are
+  // images of disjoint tile-bit sets), x ^ a = (x ^ (a & WM)) + (a & ~WM),
+  // so one pointer per distinct low part serves every element and each
+  // access is an LDS/STS with an immediate offset (option shm_addr_split;
+  // otherwise the XOR and the scaling are recomputed per element).
+  const bool asplit = C->opt.shm_addr_split != 0;
+  int agroup = 0;
+  auto addr_group = [&](const std::string &x, const std::vector<int> &as, const char *ind) {
+    std::vector<std::string> out;
+    if (!asplit) {
+      for (int a : as) out.push_back("tb[" + x + " ^ " + std::to_string(a) + "]");
+      return out;
+    }
+    std::map<int, std::string> ptr;
+    for (int a : as) {
+      const int lo = a & (int)WM, hi = a & ~(int)WM;
+      auto it = ptr.find(lo);
+      if (it == ptr.end()) {
+        const std::string nm = "q" + std::to_string(agroup++);
+        o << ind << "T *" << nm << " = tb + (" << x << " ^ " << lo << ");\n";
+        it = ptr.emplace(lo, nm).first;
+      }
+      out.push_back(it->second + "[" + std::to_string(hi) + "]");
+    }
+    return out;
+  };
 
   const int last = sl.nphase - 1;
   const bool ld = sl.last_direct != 0;
@@ -712,6 +828,25 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   const std::string next_issue =
       pipe ? "{ const u64 nx = blockIdx.x + (u64)(i + 3) * G; if (nx < " + NTL + ") issue(b, mb < 3 ? mb + 3 : mb - 3, tile_base(nx)); }"
            : "if (!zmode) { const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
+  // zero tiles (zmode): the input of this launch is |0...0> on this rank
+  // (zmode 2) or all zeros (zmode 1), so every tile except tile 0 of rank 0
+  // holds zeros; every op of the launch is linear and keeps a tile inside its
+  // own tile (a shared-memory kernel touches active qubits only), so such a
+  // tile's output is exactly zero: it is stored as zeros with none of the
+  // phases (one write-only pass instead of a full compute pass).  The pipe
+  // ring still gets its arrival for tile i + 3.
+  std::string zero_tile;
+  {
+    std::ostringstream z;
+    z << "    if (zmode && (zmode == 1 || tile != 0)) {\n";
+    z << (operm ? "      T *g = dst + obase + ooff_t;\n" : "      T *g = st + base + off_t;\n");
+    z << "      T zz; zz.x = 0; zz.y = 0;\n";
+    for (int it = 0; it < NE; it++) z << "      g[" << u64lit(PB(itoff[it])) << "] = zz;\n";
+    if (pipe) z << "      " << next_issue << "\n";
+    if (NB) z << "      itp ^= 1;\n";
+    z << "      continue;\n    }\n";
+    zero_tile = z.str();
+  }
   if (pipe) {
     // tiles i = 0, 1, 2 of this CTA's sequence into buffers 0, 1, 2, each
     // issued by the group that will process it (i & 1)
@@ -732,11 +867,13 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     if (operm) o << "    const u64 obase = otile_base(tile);\n";
     o << "    const int b = mb < 3 ? mb : mb - 3;\n";
     o << "    mbar_wait(mbar0 + 8 * mb, (i / 6) & 1);\n";
+    o << zero_tile;
   } else {
   o << "  int b = 0;\n";
   o << "  for (; tile < " << NTL << "; tile += G) {\n";
   o << "    const u64 base = tile_base(tile);\n";
   if (operm) o << "    const u64 obase = otile_base(tile);\n";
+  if (early) o << zero_tile;
   const int nwarps = BT / 32;
   for (auto &kv : bslot) {
     const int bk = kv.second;
@@ -796,17 +933,19 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "    { // phase " << p << "\n";
     o << "      const u32 jj = jtab[" << jslot[p] * NT << " + tid]; const int jt = (int)(jj & 0xffffu); "
       << "const int sj = (int)(jj >> 16); (void)jt;\n";
-    for (int e = 0; e < NE; e++) {
-      int a = 0;
-      for (int i = 0; i < RB; i++)
-        if ((e >> i) & 1) a ^= sr[i];
-      if (early && p == 0 && e == 0) o << "      if (zmode) {\n";
-      if (early && p == 0 && e == 0) {
+    {
+      std::vector<int> as(NE, 0);
+      for (int e = 0; e < NE; e++)
+        for (int i = 0; i < RB; i++)
+          if ((e >> i) & 1) as[e] ^= sr[i];
+      if (early && p == 0) {
+        o << "      if (zmode) {\n";
         for (int e2 = 0; e2 < NE; e2++) o << "        v[" << e2 << "].x = 0; v[" << e2 << "].y = 0;\n";
         o << "        if (zmode == 2 && tile == 0 && jt == 0) v[0].x = 1;\n      } else {\n";
       }
-      o << "      v[" << e << "] = tb[sj ^ " << a << "];\n";
-      if (early && p == 0 && e == NE - 1) o << "      }\n";
+      const auto ax = addr_group("sj", as, "      ");
+      for (int e = 0; e < NE; e++) o << "      v[" << e << "] = " << ax[e] << ";\n";
+      if (early && p == 0) o << "      }\n";
     }
     if (early && ld && p == last) o << "      " << GS << "\n      " << next_issue << "\n";
     for (int oi = P.op_begin; oi < P.op_end; oi++) {
@@ -1091,24 +1230,29 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
         o << "      tb[s0 ^ " << a << "] = v[" << e << "];\n";
       }
     } else {
-      for (int e = 0; e < NE; e++) {
-        int a = 0;
+      std::vector<int> as(NE, 0);
+      for (int e = 0; e < NE; e++)
         for (int i = 0; i < RB; i++)
-          if ((e >> i) & 1) a ^= sr[i];
-        o << "      tb[sj ^ " << a << "] = v[" << e << "];\n";
-      }
+          if ((e >> i) & 1) as[e] ^= sr[i];
+      const auto ax = addr_group("sj", as, "      ");
+      for (int e = 0; e < NE; e++) o << "      " << ax[e] << " = v[" << e << "];\n";
     }
     o << "      " << GS << "\n    }\n";
   }
   if (!ld) {
     o << (operm ? "    { T *g = dst + obase + ooff_t;\n" : "    { T *g = st + base + off_t;\n");
     if (early) {
-      for (int it = 0; it < NE; it++) o << "      v[" << it << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
+      std::vector<int> as;
+      for (int it = 0; it < NE; it++) as.push_back((int)Sx(SO, (unsigned)(it * NT)));
+      const auto ax = addr_group("sw_out", as, "      ");
+      for (int it = 0; it < NE; it++) o << "      v[" << it << "] = " << ax[it] << ";\n";
       o << "      " << GS << "\n      " << next_issue << "\n";
       for (int it = 0; it < NE; it++) o << "      g[" << u64lit(PB(itoff[it])) << "] = v[" << it << "];\n";
     } else {
-      for (int it = 0; it < NE; it++)
-        o << "      g[" << u64lit(PB(itoff[it])) << "] = tb[sw_out ^ " << Sx(SO, (unsigned)(it * NT)) << "];\n";
+      std::vector<int> as;
+      for (int it = 0; it < NE; it++) as.push_back((int)Sx(SO, (unsigned)(it * NT)));
+      const auto ax = addr_group("sw_out", as, "      ");
+      for (int it = 0; it < NE; it++) o << "      g[" << u64lit(PB(itoff[it])) << "] = " << ax[it] << ";\n";
     }
     o << "    }\n";
   }
