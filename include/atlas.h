@@ -216,6 +216,12 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
+ *   "zero_skip"      1 = a run that starts from |0...0> tracks the local
+ *                    slots no launch has made active yet (they are still 0):
+ *                    an in-place plan-specialised shared-memory launch does
+ *                    not visit the tiles with a 1 on such a slot (zeros in,
+ *                    zeros out), and a shard that is all zero skips its
+ *                    launches until the first remap [1]
  *   "shm_addr_split" plan-specialised kernels address a phase's shared-memory
  *                    elements as (x ^ low) + high: one pointer per distinct
  *                    low (bank-bit) part, immediate offsets for the rest [1]

@@ -87,6 +87,7 @@ struct Options {
   int shm_const_pool = 0;    // JIT fp64: coefficients in a __constant__ table (c[] operands, no UMOV)
   int shm_addr_split = 1;    // JIT: shared-memory addresses as (x ^ low) + high (immediate offsets)
   int shm_lit_smem = 0;      // JIT fp64: diagonal-run element factors read from a shared-memory table
+  int zero_skip = 1;         // runs from |0...0>: tiles provably zero in and out are not visited
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter
   long long dp_budget = 250000;
   std::string cost_model;

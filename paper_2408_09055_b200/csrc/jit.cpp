@@ -647,7 +647,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
          "%0, 1, 0, p; }\" : \"=r\"(ok) : \"r\"(a), \"r\"(par) : \"memory\"); } while (!ok); }\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
-    << "(T *__restrict__ st, T *dst, int zmode) {\n";
+    << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
   o << "//@LT_DECL@\n";
@@ -664,8 +664,11 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "  const int tid = threadIdx.x;\n";
   }
   // tile-base deposit tables
+  // nact (launch argument): the non-active slots the tiles run over -- all of
+  // them, or fewer when the caller knows the tiles with a 1 on some of them
+  // hold zeros in and out (runtime.cu, zero-support tracking); ntl = 2^|nact|
   o << "  for (int i = threadIdx.x; i < " << nbt * 256 << "; i += " << BT << ") { const int c = i >> 8; u64 m = "
-    << u64lit(sl.nonactive) << "; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
+    << "nact; for (int k = 0; k < 8 * c && m; k++) m &= m - 1; btab[i] = "
     << "pdep64((u64)(i & 255), m); }\n";
   if (operm) {
     o << "  u64 *obtab = btab + " << nbt * 256 << ";\n";
@@ -813,9 +816,9 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   }
   if (pipe) {
     o << "  const u64 G = gridDim.x;\n";
-    o << "  if ((u64)blockIdx.x >= " << u64lit(sl.ntiles) << ") return;\n";
+    o << "  if ((u64)blockIdx.x >= " << "ntl" << ") return;\n";
   } else {
-    o << "  u64 tile = blockIdx.x;\n  if (tile >= " << u64lit(sl.ntiles) << ") return;\n";
+    o << "  u64 tile = blockIdx.x;\n  if (tile >= " << "ntl" << ") return;\n";
     o << "  const u64 G = gridDim.x;\n";
   }
   // early = one tile buffer: the next tile's load is issued as soon as every
@@ -824,7 +827,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // phase's arithmetic and the HBM stores; the other CTA of the SM covers
   // the rest.
   const bool early = nbuf == 1;
-  const std::string NTL = u64lit(sl.ntiles);
+  const std::string NTL = "ntl";
   const std::string next_issue =
       pipe ? "{ const u64 nx = blockIdx.x + (u64)(i + 3) * G; if (nx < " + NTL + ") issue(b, mb < 3 ? mb + 3 : mb - 3, tile_base(nx)); }"
            : "if (!zmode) { const u64 nx = tile + G; if (nx < " + NTL + ") issue_load(0, tile_base(nx)); }";
@@ -1383,7 +1386,10 @@ static int g_nsms = 0;
 
 bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->zero_ok; }
 
-cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode) {
+// skip: non-active slots whose tiles with a 1 there are zero in and out (the
+// launch runs in place); those tiles are not visited at all
+cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
+                           uint64_t skip) {
   JitEntry *E = (JitEntry *)jit;
   const int NT = E->threads > 0 ? E->threads : 1 << (sl.K - sl.RB);
   if (E->attr_set < E->smem) {
@@ -1402,10 +1408,12 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
     cudaDeviceGetAttribute(&g_nsms, cudaDevAttrMultiProcessorCount, dev);
     if (g_nsms <= 0) g_nsms = 148;
   }
+  uint64_t nact = sl.nonactive & ~skip;
+  uint32_t ntl = (uint32_t)(sl.ntiles >> __builtin_popcountll(sl.nonactive & skip));
   uint64_t grid = (uint64_t)g_nsms * E->nt;
-  if (grid > sl.ntiles) grid = sl.ntiles;
+  if (grid > ntl) grid = ntl;
   if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
-  void *args[] = {&st, &dst, &zmode};
+  void *args[] = {&st, &dst, &zmode, &nact, &ntl};
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);
 }

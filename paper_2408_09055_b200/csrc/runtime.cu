@@ -34,7 +34,8 @@ cudaError_t launch_xor_swap(int dtype, void *st, int L, uint64_t F, cudaStream_t
 cudaError_t launch_swap_regions(int dtype, void *a, void *b, uint64_t n, cudaStream_t s);
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
 void shm_jit_prepare(atlas_ctx *C);
-cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode);
+cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
+                           uint64_t skip);
 bool shm_jit_zero_ok(const void *jit);
 
 #define CK(x)                                                                              \
@@ -444,7 +445,7 @@ static void run_offload(atlas_ctx *C) {
             const bool operm = sl.out_perm_off >= 0;
             void *dst = operm ? C->d_work[w ^ 1] : st;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z));
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z, 0));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                             (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
@@ -550,6 +551,24 @@ void run(atlas_ctx *C) {
   }
   if (!C->opt.init && !C->state_set) fail(ATLAS_E_ORDER, "option init=0 but no atlas_set_state");
   C->state_set = false;
+  // zero-support tracking (option zero_skip): a run that starts from
+  // |0...0> keeps every local slot that no launch has made active yet at 0,
+  // so a tile with a 1 on such a slot holds zeros, and an in-place
+  // shared-memory launch maps it to zeros (every op is linear and keeps a
+  // tile inside itself): those tiles are not visited.  zq[s] = the slots
+  // still known zero on slot s (all of them on ranks whose shard starts all
+  // zero: every launch there is skipped until the first exchange).  Tracking
+  // stops at the first launch it does not model (fused, interpreter, fused
+  // pack) and at the first remap.
+  const uint64_t lmask = C->L >= 64 ? ~0ull : (1ull << C->L) - 1;
+  std::vector<uint64_t> zq(C->nslots, 0);
+  std::vector<bool> zall(C->nslots, false);
+  if (C->opt.zero_skip)
+    for (int s = 0; s < C->nslots; s++)
+      if (zmode[s]) {
+        zq[s] = lmask;
+        zall[s] = zmode[s] == 1;
+      }
   const int S = C->sp.s;
   std::vector<size_t> pc(C->nslots, 0);
   const double2 *mats = (const double2 *)C->d_mats;
@@ -576,6 +595,8 @@ void run(atlas_ctx *C) {
       if (C->opt.inplace_remap) exchange_inplace(C, k);
       else do_exchange(C, k);
       mark_end();
+      std::fill(zq.begin(), zq.end(), 0);
+      std::fill(zall.begin(), zall.end(), false);
     }
     for (int s = 0; s < C->nslots; s++) {
       auto &P = C->prog[s];
@@ -584,7 +605,26 @@ void run(atlas_ctx *C) {
         void *st = cur_buf(C, s);
         // a launch that synthesises |0...0> only writes the shard
         const int zm = (k == 0 && pc[s] == 1 && ln.type == L_SHM && ln.jit) ? zmode[s] : 0;
-        mark(ln.type, zm ? ln.bytes / 2 : ln.bytes);
+        // zero tiles of this launch (see zq above)
+        uint64_t skip = 0;
+        if (!zm && zq[s]) {
+          if (ln.type == L_SHM && ln.jit && ln.sl.out_perm_off < 0) {
+            if (zall[s]) continue;  // the whole shard is zero: nothing to do
+            skip = zq[s] & ln.sl.nonactive;
+          } else {
+            zq[s] = 0;
+            zall[s] = false;
+          }
+        }
+        if (ln.type == L_SHM && zq[s]) zq[s] &= ln.sl.nonactive;  // active slots may turn nonzero
+        if (zm || skip) {
+          // algorithmic bytes of the tiles visited (write-only from |0...0>)
+          const int64_t vis = (int64_t)(ln.sl.ntiles >> __builtin_popcountll(skip));
+          const int64_t b = (int64_t)((double)ln.bytes * (double)vis / (double)ln.sl.ntiles);
+          mark(ln.type, zm ? ln.bytes / 2 : b);
+        } else {
+          mark(ln.type, ln.bytes);
+        }
         switch (ln.type) {
           case L_FUSED: CK(launch_fused(dt, st, C->L, ln.fl, mats, C->stream)); break;
           case L_SHM: {
@@ -594,7 +634,7 @@ void run(atlas_ctx *C) {
             const bool operm = sl.out_perm_off >= 0;
             void *dst = operm ? other_buf(C, s) : st;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm));
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm, skip));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                             (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
