@@ -219,6 +219,51 @@ const int kDiagSel[11] = {0, 1, 2, 4, 8, 3, 5, 9, 6, 10, 12};
 int shm_nbuf_effective(int dtype, const ShmLaunch &sl);
 size_t shm_jit_smem(const std::string &src);
 
+// TMA tile loads (option shm_tma, fp64 pipe kernels).  The shard is viewed
+// as a tensor of at most 5 dimensions, each a run of consecutive local slots
+// whose low part is active (covered by the box) and whose high part is
+// non-active (selected by the tile's coordinates): dim 0 = slots 0..2 (8
+// amplitudes = 16 doubles = one 128-B swizzle row), then greedy runs of at
+// most 8 active slots followed by the non-active slots up to the next
+// active one.  One cp.async.bulk.tensor per tile moves all 2^K amplitudes
+// into shared memory with the 128-B swizzle (16-B chunk index ^= row index
+// mod 8, i.e. tile index j -> j ^ ((j >> 3) & 7)), completing on the tile's
+// mbarrier.  Launches whose active slots need more than 5 runs, or do not
+// include slots 0..2, keep the per-thread cp.async gather.
+struct TmaDims {
+  int rank = 0;
+  int start[5], len[5], abits[5];
+};
+static bool tma_dims(const ShmLaunch &sl, TmaDims &d) {
+  const int L = sl.K + __builtin_popcountll(sl.nonactive);
+  uint64_t act = 0;
+  for (int b = 0; b < sl.K; b++) act |= 1ull << sl.act[b];
+  if ((act & 7) != 7 || sl.K < 6) return false;
+  d.rank = 1;
+  d.start[0] = 0;
+  d.len[0] = 3;
+  d.abits[0] = 3;
+  int cur = 3;
+  while (cur < L) {
+    if (d.rank == 5) return false;
+    const int s0 = cur;
+    int a = 0;
+    while (cur < L && ((act >> cur) & 1) && a < 8) {
+      cur++;
+      a++;
+    }
+    while (cur < L && !((act >> cur) & 1)) cur++;
+    if (cur - s0 > 31) return false;
+    d.start[d.rank] = s0;
+    d.len[d.rank] = cur - s0;
+    d.abits[d.rank] = a;
+    d.rank++;
+  }
+  return true;
+}
+thread_local bool g_no_tma = false;
+struct TmaRetry {};
+
 // The straight-line source of one shared-memory launch (same skeleton as
 // kernels.cu shm_kernel: ring of tile buffers filled with cp.async, register
 // phases, permuted stores, optional direct HBM store of the last phase).
@@ -278,18 +323,28 @@ std::string shm_jit_source(const atlas_ctx *C, const ShmLaunch &sl, const std::s
   std::string body;
   try {
     g_ltab = use_tab ? &tab : nullptr;
-    body = shm_jit_source_body(C, sl, name);
+    g_no_tma = false;
+    try {
+      body = shm_jit_source_body(C, sl, name);
+    } catch (const TmaRetry &) {  // TMA needs the pipe pipeline; it was not chosen
+      g_no_tma = true;
+      tab = LitTab();
+      pool = LitPool();
+      body = shm_jit_source_body(C, sl, name);
+    }
     g_ltab = nullptr;
     std::string patched = patch_lit_table(body, tab);
     if (patched.empty()) {  // the table does not fit: literals
       pool = LitPool();
       body = patch_lit_table(shm_jit_source_body(C, sl, name), LitTab());
+      g_no_tma = false;
     } else {
       body = patched;
     }
   } catch (...) {
     g_pool = nullptr;
     g_ltab = nullptr;
+    g_no_tma = false;
     throw;
   }
   g_pool = nullptr;
@@ -350,6 +405,15 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   typedef std::vector<unsigned> Swz;
   std::vector<Swz> swzs(1, Swz(K, 0));
   for (int b = W; b < K; b++) swzs[0][b] = 1u << (b % W);
+  // the lowering (plan.cpp) stores its tile vectors under the global swizzle
+  // GL (device.h); the layout of the tile load (swzs[0]) is GL for the
+  // cp.async gather, the 128-B TMA swizzle for TMA loads
+  const Swz GL = swzs[0];
+  TmaDims tdim;
+  const bool tma = !f32 && nbuf == 1 && C->opt.shm_tma && C->opt.shm_pipe && !g_no_tma &&
+                   (1 << (K - RB)) * 2 <= 512 && tma_dims(sl, tdim);
+  if (tma)
+    for (int b = W; b < K; b++) swzs[0][b] = b < 2 * W ? 1u << (b - W) : 0u;
   auto Sx = [&](const Swz &c, unsigned j) {
     unsigned r = j;
     for (int b = W; b < K; b++)
@@ -381,8 +445,8 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   for (int p = 0; p < sl.nphase; p++)
     if (ph[p].permuted) {
       Acol[p].resize(K);
-      for (int b = 0; b < K; b++) Acol[p][b] = Sx(swzs[0], ph[p].colimg[b]);
-      Ac0[p] = Sx(swzs[0], ph[p].c0_swz);
+      for (int b = 0; b < K; b++) Acol[p][b] = Sx(GL, ph[p].colimg[b]);
+      Ac0[p] = Sx(GL, ph[p].c0_swz);
     }
   const int lastp = sl.nphase - 1;
   const bool ld_ = sl.last_direct != 0;
@@ -603,6 +667,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // registers measured slower than two single-buffer CTAs)
   bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 512 &&
               layout(3, off_jtab, off_stab, off_btab, off_mbar) + 1024 <= 233472;
+  if (tma && !pipe) throw TmaRetry();
   // the thread-factor table must not cost occupancy (or exceed the opt-in
   // limit): drop slots until it fits beside the resident CTAs
   if (pipe) minb = 1;
@@ -628,14 +693,15 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "typedef unsigned long long u64; typedef unsigned int u32; typedef unsigned short u16;\n";
   o << (f32 ? "typedef float R; typedef float2 T;\n" : "typedef double R; typedef double2 T;\n");
   o << "#define SMEM_BYTES " << smem << "\n";
+  if (tma) {
+    o << "#define ATLAS_TMA " << tdim.rank;
+    for (int d = 0; d < tdim.rank; d++) o << " " << tdim.start[d] << ":" << tdim.len[d] << ":" << tdim.abits[d];
+    o << "\nstruct __align__(64) TMap { unsigned long long v[16]; };\n";
+  }
   // zmode (early pipeline only): 1 = the input is all zeros, 2 = the input
   // is |0...0> on this rank (atlas_run's initial state): the first tile
   // load is synthesised in registers and nothing is read from HBM
   o << "#define ZERO_OK " << (nbuf == 1 ? 1 : 0) << "\n";
-  o << "__device__ __forceinline__ int swz(int j) { return "
-    << (f32 ? "j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15)"
-            : "j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7)")
-    << "; }\n";
   o << "__device__ __forceinline__ u64 pdep64(u64 v, u64 mask) { u64 r = 0; while (mask) { u64 lo = "
        "mask & (~mask + 1); if (v & 1) r |= lo; v >>= 1; mask ^= lo; } return r; }\n";
   o << "#define BLOCK_THREADS " << BT << "\n";
@@ -647,8 +713,9 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
          "%0, 1, 0, p; }\" : \"=r\"(ok) : \"r\"(a), \"r\"(par) : \"memory\"); } while (!ok); }\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
-    << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl) {\n";
-  o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
+    << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl"
+    << (tma ? ", const __grid_constant__ TMap tmap" : "") << ") {\n";
+  o << "  extern __shared__ __align__(1024) unsigned char smraw[];\n";
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
   o << "//@LT_DECL@\n";
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
@@ -658,8 +725,11 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   if (pipe) {
     o << "  const int tid = threadIdx.x & " << NT - 1 << ", grp = threadIdx.x / " << NT << ";\n";
     o << "  const unsigned mbar0 = (unsigned)__cvta_generic_to_shared(smraw + " << off_mbar << ");\n";
-    o << "  if (threadIdx.x == 0) for (int i = 0; i < 6; i++) asm volatile(\"mbarrier.init.shared::cta.b64 "
-         "[%0], %1;\" :: \"r\"(mbar0 + 8 * i), \"r\"(" << NT << ") : \"memory\");\n";
+    // TMA: one arrival (with the transaction bytes) per tile; cp.async: one
+    // per thread of the group
+    o << "  if (threadIdx.x == 0) { for (int i = 0; i < 6; i++) asm volatile(\"mbarrier.init.shared::cta.b64 "
+         "[%0], %1;\" :: \"r\"(mbar0 + 8 * i), \"r\"(" << (tma ? 1 : NT) << ") : \"memory\");"
+      << (tma ? " asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");" : "") << " }\n";
   } else {
     o << "  const int tid = threadIdx.x;\n";
   }
@@ -737,7 +807,9 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "\n  u64 ooff_t = 0;";
     for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) ooff_t |= " << u64lit(PB(1ull << sl.act[i])) << ";";
   }
-  o << "\n  const int sw_tid = swz(tid);\n";
+  o << "\n  int sw_tid = 0;";
+  for (int t = 0; t < K - RB; t++) o << " if ((tid >> " << t << ") & 1) sw_tid ^= " << Sx(swzs[0], 1u << t) << ";";
+  o << "\n";
   // copy-out reads the layout of the last boundary
   const Swz &SO = swzs[ssw[lastp]];
   o << "  int sw_out = 0;";
@@ -765,7 +837,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "  auto issue_load = [&](int bsel, " << (pipe ? "int msel, " : "") << "u64 base) {\n    const T *g = st + base + off_t;\n";
   for (int it = 0; it < NE; it++) {
     o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (sw_tid ^ "
-      << swz(it * NT) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
+      << Sx(swzs[0], (unsigned)(it * NT)) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
     if (!f32) o << "asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
     else o << "asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
   }
@@ -774,9 +846,31 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   else
     o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n  };\n";
   // pipe, zero mode: the ring protocol without data (plain arrivals)
-  if (pipe)
+  if (pipe && !tma)
     o << "  auto issue = [&](int bsel, int msel, u64 base) { if (!zmode) issue_load(bsel, msel, base); else asm volatile("
          "\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mbar0 + 8 * msel) : \"memory\"); };\n";
+  if (tma) {
+    // one thread of the group: the tile's coordinates from its base, one
+    // bulk tensor copy completing on the tile's mbarrier (expect_tx)
+    o << "  const u64 tmap_a = reinterpret_cast<u64>(&tmap);\n";
+    o << "  auto issue = [&](int bsel, int msel, u64 base) {\n    if (tid != 0) return;\n"
+      << "    const unsigned mb_ = mbar0 + 8 * msel;\n"
+      << "    if (zmode) { asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mb_) : \"memory\"); return; }\n"
+      << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+      << "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(mb_), \"r\"("
+      << (TILE * esz) << ") : \"memory\");\n";
+    o << "    const int c0 = 0";
+    for (int d = 1; d < tdim.rank; d++)
+      o << ", c" << d << " = (int)((base >> " << tdim.start[d] << ") & " << u64lit((1ull << tdim.len[d]) - 1) << ")";
+    o << ";\n";
+    o << "    asm volatile(\"cp.async.bulk.tensor." << tdim.rank
+      << "d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {";
+    for (int d = 0; d < tdim.rank; d++) o << (d ? ", " : "") << "%" << (2 + d);
+    o << "}], [%" << (2 + tdim.rank) << "];\" :: \"r\"(sm_base + (unsigned)bsel * " << (TILE * esz)
+      << "u), \"l\"(tmap_a)";
+    for (int d = 0; d < tdim.rank; d++) o << ", \"r\"(c" << d << ")";
+    o << ", \"r\"(mb_) : \"memory\");\n  };\n";
+  }
   const std::string GS = pipe ? "gsync(grp);" : "__syncthreads();";
   // tb[x ^ a] for one thread part x and the element constants a of a phase:
   // when x's set bits above the bank bits (W) never meet a's (x and a are
@@ -1223,7 +1317,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       o << "      u32 cb = " << Sx(swzs[ssw[p]], Ac0[p]) << "u;\n";
       for (int i = P.term_begin; i < P.term_end; i++)
         o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
-          << ") cb ^= " << Sx(swzs[ssw[p]], Sx(swzs[0], terms[i].vec_swz)) << "u;\n";
+          << ") cb ^= " << Sx(swzs[ssw[p]], Sx(GL, terms[i].vec_swz)) << "u;\n";
       o << "      const int s0 = (int)(stab[" << sslot[p] * NT << " + tid] ^ cb);\n";
       o << "      " << GS << "\n";
       for (int e = 0; e < NE; e++) {
