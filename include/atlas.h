@@ -222,6 +222,11 @@ const char *atlas_last_error(void);
  *                    not visit the tiles with a 1 on such a slot (zeros in,
  *                    zeros out), and a shard that is all zero skips its
  *                    launches until the first remap [1]
+ *   "shm_tma"        plan-specialised fp64 kernels of the two-group pipeline
+ *                    load each tile with one TMA tensor copy
+ *                    (cp.async.bulk.tensor, 128-B swizzle, mbarrier
+ *                    transaction count) instead of 16 cp.async per thread,
+ *                    when the launch's local slots form <= 5 runs [1]
  *   "shm_addr_split" plan-specialised kernels address a phase's shared-memory
  *                    elements as (x ^ low) + high: one pointer per distinct
  *                    low (bank-bit) part, immediate offsets for the rest [1]

@@ -17,6 +17,7 @@
 // NVRTC is loaded at run time (libnvrtc.so.12 from the CUDA toolkit of this
 // image); the cubin is loaded with cudaLibraryLoadData.  Identical sources
 // are compiled once per process.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -89,6 +90,10 @@ struct JitEntry {
   cudaKernel_t kern = nullptr;
   int smem = 0, nt = 0, attr_set = 0, threads = 0;
   bool zero_ok = false;
+  // TMA tile loads: the tensor dimensions the kernel was generated for
+  // (runs of local slots: start, length, active low bits)
+  int tma_rank = 0;
+  int tstart[5] = {0}, tlen[5] = {0}, tabits[5] = {0};
 };
 std::mutex g_cache_mu;
 std::unordered_map<std::string, JitEntry *> g_cache;  // source -> compiled kernel
@@ -1440,6 +1445,15 @@ static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &s
     e = cudaLibraryGetKernel(&E->kern, E->lib, names[i].c_str());
     if (e != cudaSuccess) fail(ATLAS_E_CUDA, "cudaLibraryGetKernel: %s", cudaGetErrorString(e));
     E->smem = (int)shm_jit_smem(srcs[i]);
+    if (const char *tp = strstr(srcs[i].c_str(), "#define ATLAS_TMA ")) {
+      tp += 18;
+      E->tma_rank = (int)strtol(tp, (char **)&tp, 10);
+      for (int d = 0; d < E->tma_rank; d++) {
+        E->tstart[d] = (int)strtol(tp, (char **)&tp, 10);
+        E->tlen[d] = (int)strtol(tp + 1, (char **)&tp, 10);
+        E->tabits[d] = (int)strtol(tp + 1, (char **)&tp, 10);
+      }
+    }
     E->zero_ok = shm_jit_zero_ok_src(srcs[i]);
     {
       const char *p = strstr(srcs[i].c_str(), "#define BLOCK_THREADS ");
@@ -1502,12 +1516,42 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
     cudaDeviceGetAttribute(&g_nsms, cudaDevAttrMultiProcessorCount, dev);
     if (g_nsms <= 0) g_nsms = 148;
   }
+  // TMA: the shard (the launch reads st) as a <= 5-dimensional fp64 tensor
+  // whose dimensions are the runs of local slots of the generated kernel
+  // (tma_dims); the box is the tile, 128-B swizzled
+  alignas(64) CUtensorMap tmap;
+  if (E->tma_rank) {
+    typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+    static EncodeTiled enc = nullptr;
+    if (!enc) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+      if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+      enc = (EncodeTiled)fn;
+    }
+    cuuint64_t gdim[5], gstr[4];
+    cuuint32_t box[5], es[5];
+    for (int d = 0; d < E->tma_rank; d++) {
+      gdim[d] = d == 0 ? 16 : (cuuint64_t)1 << E->tlen[d];
+      box[d] = d == 0 ? 16 : 1u << E->tabits[d];
+      es[d] = 1;
+      if (d > 0) gstr[d - 1] = (cuuint64_t)16 << E->tstart[d];
+    }
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)E->tma_rank, st, gdim, gstr, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
   uint64_t nact = sl.nonactive & ~skip;
   uint32_t ntl = (uint32_t)(sl.ntiles >> __builtin_popcountll(sl.nonactive & skip));
   uint64_t grid = (uint64_t)g_nsms * E->nt;
   if (grid > ntl) grid = ntl;
   if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
-  void *args[] = {&st, &dst, &zmode, &nact, &ntl};
+  void *args[] = {&st, &dst, &zmode, &nact, &ntl, &tmap};
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);
 }
