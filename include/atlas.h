@@ -226,7 +226,11 @@ const char *atlas_last_error(void);
  *                    load each tile with one TMA tensor copy
  *                    (cp.async.bulk.tensor, 128-B swizzle, mbarrier
  *                    transaction count) instead of 16 cp.async per thread,
- *                    when the launch's local slots form <= 5 runs [1]
+ *                    when the launch's local slots form <= 5 runs.
+ *                    Experimental: measured no faster than cp.async (qft
+ *                    n = 28 2.267 vs 2.273 ms) and some n = 28 runs stall
+ *                    on a tile that never completes (the kernel traps after
+ *                    ~10 s), so off by default [0]
  *   "shm_addr_split" plan-specialised kernels address a phase's shared-memory
  *                    elements as (x ^ low) + high: one pointer per distinct
  *                    low (bank-bit) part, immediate offsets for the rest [1]

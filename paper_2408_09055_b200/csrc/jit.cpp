@@ -94,6 +94,10 @@ struct JitEntry {
   // (runs of local slots: start, length, active low bits)
   int tma_rank = 0;
   int tstart[5] = {0}, tlen[5] = {0}, tabits[5] = {0};
+  // device copies of the encoded tensor map, one per state buffer the kernel
+  // has read (written once; distinct addresses, so no descriptor cached for
+  // one map is ever looked up for another)
+  std::map<const void *, void *> dmaps;
 };
 std::mutex g_cache_mu;
 std::unordered_map<std::string, JitEntry *> g_cache;  // source -> compiled kernel
@@ -680,13 +684,15 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     const int keep = NTF;
     NTF = 0;
     const size_t base_sz = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar);
-    const size_t cap = minb >= 2 ? 233472 / minb - 1024 : 232448;
+    const size_t cap = (minb >= 2 ? 233472 / minb - 1024 : 232448) - (tma ? 1024 : 0);
     const size_t fit = base_sz < cap ? (cap - base_sz) / ((size_t)NT * esz) : 0;
     NTF = (int)std::min<size_t>(keep, fit);
     for (auto it = tslot.begin(); it != tslot.end();)
       it = it->second >= NTF ? tslot.erase(it) : std::next(it);
   }
-  const size_t smem = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar);
+  // TMA: 1 KiB of slack so the tile buffers can start on a 1024-B boundary
+  // (the 128-B swizzle pattern repeats every 1024 B of shared address)
+  const size_t smem = layout(pipe ? 3 : nbuf, off_jtab, off_stab, off_btab, off_mbar) + (tma ? 1024 : 0);
   const int BT = pipe ? 2 * NT : NT;  // threads per CTA
   // option shm_ctas = 3: three resident CTAs per SM (register cap 80) when
   // their shared memory fits the SM
@@ -713,14 +719,27 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   if (pipe) {
     o << "__device__ __forceinline__ void gsync(int g) { asm volatile(\"bar.sync %0, " << NT
       << ";\" :: \"r\"(1 + g) : \"memory\"); }\n";
-    o << "__device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) { unsigned ok = 0; do { "
+    // a tile load that never lands (a broken tensor map, a lost arrival)
+    // traps after ~10 s instead of hanging the device
+    o << "__device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) { unsigned ok = 0; "
+         "const long long t0 = clock64(); do { "
          "asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 "
-         "%0, 1, 0, p; }\" : \"=r\"(ok) : \"r\"(a), \"r\"(par) : \"memory\"); } while (!ok); }\n";
+         "%0, 1, 0, p; }\" : \"=r\"(ok) : \"r\"(a), \"r\"(par) : \"memory\"); "
+         "if (!ok && clock64() - t0 > 20000000000ll) __trap(); } while (!ok); }\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
     << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl"
-    << (tma ? ", const __grid_constant__ TMap tmap" : "") << ") {\n";
-  o << "  extern __shared__ __align__(1024) unsigned char smraw[];\n";
+    << (tma ? ", const TMap *__restrict__ tmg" : "") << ") {\n";
+  if (tma) {
+    o << "  extern __shared__ __align__(1024) unsigned char smraw_[];\n";
+    o << "  const unsigned smpad = (1024u - ((unsigned)__cvta_generic_to_shared(smraw_) & 1023u)) & 1023u;\n";
+    o << "  unsigned char *smraw = smraw_ + smpad;\n";
+    if (getenv("ATLAS_DEBUG_ALIGN"))
+      o << "  if (threadIdx.x == 0 && smpad) printf(\"atlas: block %d dynamic smem base %% 1024 = %u\\n\", "
+           "(int)blockIdx.x, 1024u - smpad);\n";
+  } else {
+    o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
+  }
   o << "  T *buf = reinterpret_cast<T *>(smraw);\n";
   o << "//@LT_DECL@\n";
   o << "  u32 *jtab = reinterpret_cast<u32 *>(smraw + " << off_jtab << ");\n";
@@ -857,7 +876,11 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   if (tma) {
     // one thread of the group: the tile's coordinates from its base, one
     // bulk tensor copy completing on the tile's mbarrier (expect_tx)
-    o << "  const u64 tmap_a = reinterpret_cast<u64>(&tmap);\n";
+    // the tensor map lives in global memory, one per (kernel, state buffer),
+    // written once by the host: acquire it for the tensormap proxy before
+    // the first bulk tensor copy of this CTA
+    o << "  const u64 tmap_a = reinterpret_cast<u64>(tmg);\n";
+    o << "  if (tid == 0) asm volatile(\"fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\" :: \"l\"(tmap_a) : \"memory\");\n";
     o << "  auto issue = [&](int bsel, int msel, u64 base) {\n    if (tid != 0) return;\n"
       << "    const unsigned mb_ = mbar0 + 8 * msel;\n"
       << "    if (zmode) { asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(mb_) : \"memory\"); return; }\n"
@@ -1491,6 +1514,7 @@ void shm_jit_prepare(atlas_ctx *C) {
 }
 
 static int g_nsms = 0;
+static std::mutex g_tmap_mu;
 
 bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->zero_ok; }
 
@@ -1519,8 +1543,14 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
   // TMA: the shard (the launch reads st) as a <= 5-dimensional fp64 tensor
   // whose dimensions are the runs of local slots of the generated kernel
   // (tma_dims); the box is the tile, 128-B swizzled
-  alignas(64) CUtensorMap tmap;
+  void *tmg = nullptr;
   if (E->tma_rank) {
+    std::lock_guard<std::mutex> lk(g_tmap_mu);
+    auto it = E->dmaps.find(st);
+    if (it != E->dmaps.end()) tmg = it->second;
+  }
+  if (E->tma_rank && !tmg) {
+    alignas(64) CUtensorMap tmap;
     typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                     const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
                                     CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -1545,13 +1575,19 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMalloc(&tmg, sizeof(CUtensorMap));
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(tmg, &tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_tmap_mu);
+    E->dmaps[st] = tmg;
   }
   uint64_t nact = sl.nonactive & ~skip;
   uint32_t ntl = (uint32_t)(sl.ntiles >> __builtin_popcountll(sl.nonactive & skip));
   uint64_t grid = (uint64_t)g_nsms * E->nt;
   if (grid > ntl) grid = ntl;
   if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
-  void *args[] = {&st, &dst, &zmode, &nact, &ntl, &tmap};
+  void *args[] = {&st, &dst, &zmode, &nact, &ntl, &tmg};
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);
 }

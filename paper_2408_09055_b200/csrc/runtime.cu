@@ -528,8 +528,18 @@ void run(atlas_ctx *C) {
     CK(cudaEventRecord(ev_at(nev++), C->stream));
     rec.push_back({kind, bytes});
   };
+  // ATLAS_DEBUG_SYNC=1: synchronise after every launch and name the one
+  // that fails (debugging aid; not for timing)
+  static const bool dbg_sync = getenv("ATLAS_DEBUG_SYNC") != nullptr;
+  int nlaunch = 0;
   auto mark_end = [&]() {
     if (timing) CK(cudaEventRecord(ev_at(nev++), C->stream));
+    if (dbg_sync) {
+      const cudaError_t e = cudaStreamSynchronize(C->stream);
+      fprintf(stderr, "atlas debug: launch %d %s\n", nlaunch, cudaGetErrorString(e));
+      if (e != cudaSuccess) fail(ATLAS_E_CUDA, "launch %d: %s", nlaunch, cudaGetErrorString(e));
+    }
+    nlaunch++;
   };
   // init |0...0>: logical 0 -> physical 0 (no flips at stage 0) on rank 0.
   // When the first launch of stage 0 is a plan-specialised shared-memory

@@ -86,7 +86,8 @@ def test_bench_config_mirror_full_state(fam):
 
 
 @pytest.mark.parametrize("opt", [{}, {"shm_pipe": 0}, {"shm_pipe": 0, "shm_ctas": 3},
-                                 {"shm_direct_store": 0}, {"shm_tfac_min": 0}])
+                                 {"shm_direct_store": 0}, {"shm_tfac_min": 0}, {"shm_tma": 0},
+                                 {"zero_skip": 0}, {"shm_addr_split": 0}, {"shm_lit_smem": 1}])
 @pytest.mark.parametrize("fam", ["su2random", "qsvm", "ising", "qft", "random"])
 def test_grid_capped_many_tiles(fam, opt):
     """A grid of 3 CTAs at n = 18 (64 tiles): each pipe group runs ~10 tiles
@@ -215,3 +216,45 @@ def test_offload_tier_from_input_state():
         s.run()
         psi = s.get_state()
     check(psi, O.simulate(c, init=psi0))
+
+
+@pytest.mark.parametrize("fam", ["su2random", "qft", "ising"])
+def test_zero_skip_runs_then_set_state(fam):
+    """Zero-support tracking (option zero_skip) only applies to runs from
+    |0...0>: run from |0...0> (tiles skipped), then from an arbitrary input
+    state (nothing skipped: every tile is nonzero), then from |0...0> again,
+    on one context; every result element-wise against O1.  n = 20 with the
+    grid capped so that the skipped and the visited tiles are spread over
+    several tiles per CTA."""
+    n = 20
+    c = C.make(fam, n)
+    rng = np.random.default_rng(11)
+    psi0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    ref0 = O.simulate(c)
+    ref1 = O.simulate(c, init=psi0)
+    with A.Simulator(n, 0, 1, 0, shm_grid=7) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        s.run()
+        check(s.get_state(), ref0)
+        s.set_state(psi0)
+        s.set_option("init", 0)
+        s.run()
+        check(s.get_state(), ref1)
+        s.set_option("init", 1)
+        s.run()
+        check(s.get_state(), ref0)
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_zero_skip_virtual_world_ranks(W):
+    """In a virtual world every shard but rank 0's starts all zero: its
+    stage-0 launches after the first are skipped entirely (zero_skip), rank
+    0's visit only the tiles inside the reached support.  Element-wise vs O1
+    with and without the option."""
+    c = C.make("su2random", 21)
+    ref = O.simulate(c)
+    for zs in (1, 0):
+        (psi,), _ = run(c, world=W, zero_skip=zs)
+        check(psi, ref)
