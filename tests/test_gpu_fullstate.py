@@ -86,7 +86,7 @@ def test_bench_config_mirror_full_state(fam):
 
 
 @pytest.mark.parametrize("opt", [{}, {"shm_pipe": 0}, {"shm_pipe": 0, "shm_ctas": 3},
-                                 {"shm_direct_store": 0}, {"shm_tfac_min": 0}, {"shm_tma": 0},
+                                 {"shm_direct_store": 0}, {"shm_tfac_min": 0},
                                  {"zero_skip": 0}, {"shm_addr_split": 0}, {"shm_lit_smem": 1}])
 @pytest.mark.parametrize("fam", ["su2random", "qsvm", "ising", "qft", "random"])
 def test_grid_capped_many_tiles(fam, opt):
