@@ -254,6 +254,17 @@ const char *atlas_last_error(void);
  *                    through a 256 MiB receive staging buffer with NCCL) --
  *                    halves the HBM a rank needs (NEXT-3: n = 36 fp64 on 8
  *                    B200s, 128 GiB shards); set before the first run [0]
+ *   "shm_fuse_exchange" the remap's exchange is fused into the previous
+ *                    stage's last shared-memory launch as well: it stores
+ *                    each packed block straight into the buffer of the rank
+ *                    it goes to -- another slot's buffer in a virtual world,
+ *                    a peer GPU's memory over NVLink (CUDA IPC handles
+ *                    exchanged over NCCL at the first run) with one process
+ *                    per GPU, followed by a 4-byte allreduce -- so no
+ *                    separate all-to-all runs.  Remaps without a pack get an
+ *                    identity pack.  Needs every slot's last launch to be a
+ *                    plan-specialised shared-memory kernel; library-owned
+ *                    buffers for one process per GPU [1]
  *   "shm_fuse_pack"  the local bit permutation ("pack") that precedes a
  *                    remap's exchange is folded into the store addresses of
  *                    the previous stage's last shared-memory launch, which

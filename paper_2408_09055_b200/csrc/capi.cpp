@@ -279,6 +279,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_tma") { o.shm_tma = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_addr_split") { o.shm_addr_split = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_lit_smem") { o.shm_lit_smem = (int)v; C->jit_ready = false; replan = false; }
+    else if (k == "shm_fuse_exchange") o.shm_fuse_exchange = (int)v;
     else if (k == "shm_fuse_pack") o.shm_fuse_pack = (int)v;
     else if (k == "offload") {
       // R regional qubits held in host DRAM: planned like a virtual world of

@@ -82,6 +82,7 @@ struct Options {
   int shm_pipe = 1;          // JIT: two thread groups per CTA on a ring of 3 tile buffers
   int shm_ctas = 2;          // JIT: resident SHM CTAs per SM for 2^12 fp64 tiles (2 or 3)
   int inplace_remap = 0;     // remaps in place (pair swaps), no scratch shard buffer (NEXT-3)
+  int shm_fuse_exchange = 1; // the fused-pack launch also stores each block into its destination rank's buffer
   int shm_fuse_pack = 1;     // the remap pack fused into the previous stage's last SHM launch
   int shm_grid = 0;          // > 0: cap every SHM launch at this many CTAs (tests: many tiles per CTA at small n)
   int shm_const_pool = 0;    // JIT fp64: coefficients in a __constant__ table (c[] operands, no UMOV)
@@ -165,5 +166,10 @@ struct atlas_ctx {
   std::vector<int> launch_kind;
   std::vector<int64_t> launch_bytes;
   void *nccl_comm = nullptr;
+  // fused exchange over peer memory (option shm_fuse_exchange, one process
+  // per GPU): every rank's state and scratch shard opened by CUDA IPC
+  bool ipc_ready = false;
+  std::vector<void *> ipc_state, ipc_scratch;  // [rank]; own rank = own buffers
+  void *d_bar = nullptr;                       // 4 B: the allreduce that ends a fused exchange
   bool state_set = false;
 };

@@ -127,6 +127,12 @@ struct ShmLaunch {
   // other buffer with local slot b moved to newpos[b] (plan-specialised
   // kernels only; the interpreter runs in place and a permute follows)
   int64_t out_perm_off;
+  // > 0 (with out_perm_off): the launch also performs the next remap's
+  // exchange (option shm_fuse_exchange): output offset y goes to
+  // peers[y >> (L - peer_gp)][y & (2^(L - peer_gp) - 1)], the 2^peer_gp
+  // destination blocks (the peers' other buffers, or this slot's own) passed
+  // as a launch argument
+  int32_t peer_gp;
 };
 
 // Fused dense kernel ("Fusion"): one 2^k x 2^k matrix on k slots.

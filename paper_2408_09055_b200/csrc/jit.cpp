@@ -389,6 +389,9 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // distributes over the XOR / OR of disjoint offsets, so every store-side
   // constant is mapped at generation time and the tile base by a table.
   const bool operm = sl.out_perm_off >= 0;
+  // fused exchange: the packed output goes to the destination ranks' buffers
+  const int pgp = operm ? sl.peer_gp : 0;
+  const int PSH = C->L - pgp;
   std::vector<int> np;
   if (operm) np.assign(C->newpos.begin() + sl.out_perm_off, C->newpos.begin() + sl.out_perm_off + C->L);
   auto PB = [&](uint64_t x) {
@@ -704,6 +707,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "typedef unsigned long long u64; typedef unsigned int u32; typedef unsigned short u16;\n";
   o << (f32 ? "typedef float R; typedef float2 T;\n" : "typedef double R; typedef double2 T;\n");
   o << "#define SMEM_BYTES " << smem << "\n";
+  if (pgp) o << "#define ATLAS_PEER " << pgp << "\nstruct PeerTab { T *p[8]; };\n";
   if (tma) {
     o << "#define ATLAS_TMA " << tdim.rank;
     for (int d = 0; d < tdim.rank; d++) o << " " << tdim.start[d] << ":" << tdim.len[d] << ":" << tdim.abits[d];
@@ -729,7 +733,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
     << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl"
-    << (tma ? ", const TMap *__restrict__ tmg" : "") << ") {\n";
+    << (tma ? ", const TMap *__restrict__ tmg" : "") << (pgp ? ", const PeerTab ptab" : "") << ") {\n";
   if (tma) {
     o << "  extern __shared__ __align__(1024) unsigned char smraw_[];\n";
     o << "  const unsigned smpad = (1024u - ((unsigned)__cvta_generic_to_shared(smraw_) & 1023u)) & 1023u;\n";
@@ -842,6 +846,9 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);\n";
   o << "//@LT_FILL@\n";
   o << "  __syncthreads();\n";
+  if (pgp)
+    o << "  auto pst = [&](u64 y) -> T & { return ptab.p[y >> " << PSH << "][y & " << u64lit((1ull << PSH) - 1)
+      << "]; };\n";
   o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255]";
   for (int c = 1; c < nbt; c++) o << " | btab[" << 256 * c << " + ((tile >> " << 8 * c << ") & 255)]";
   o << "; };\n";
@@ -964,9 +971,14 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   {
     std::ostringstream z;
     z << "    if (zmode && (zmode == 1 || tile != 0)) {\n";
-    z << (operm ? "      T *g = dst + obase + ooff_t;\n" : "      T *g = st + base + off_t;\n");
     z << "      T zz; zz.x = 0; zz.y = 0;\n";
-    for (int it = 0; it < NE; it++) z << "      g[" << u64lit(PB(itoff[it])) << "] = zz;\n";
+    if (pgp) {
+      z << "      const u64 gy = obase + ooff_t;\n";
+      for (int it = 0; it < NE; it++) z << "      pst(gy + " << u64lit(PB(itoff[it])) << ") = zz;\n";
+    } else {
+      z << (operm ? "      T *g = dst + obase + ooff_t;\n" : "      T *g = st + base + off_t;\n");
+      for (int it = 0; it < NE; it++) z << "      g[" << u64lit(PB(itoff[it])) << "] = zz;\n";
+    }
     if (pipe) z << "      " << next_issue << "\n";
     if (NB) z << "      itp ^= 1;\n";
     z << "      continue;\n    }\n";
@@ -1336,7 +1348,10 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
         uint64_t x = 0;
         for (int i = 0; i < RB; i++)
           if ((e >> i) & 1) x ^= limg[i];
-        o << "      " << (operm ? "dst[obase" : "st[base") << " | (cg ^ " << u64lit(PB(x)) << ")] = v[" << e << "];\n";
+        if (pgp)
+          o << "      pst(obase | (cg ^ " << u64lit(PB(x)) << ")) = v[" << e << "];\n";
+        else
+          o << "      " << (operm ? "dst[obase" : "st[base") << " | (cg ^ " << u64lit(PB(x)) << ")] = v[" << e << "];\n";
       }
       o << "    }\n";
       break;
@@ -1365,19 +1380,23 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "      " << GS << "\n    }\n";
   }
   if (!ld) {
-    o << (operm ? "    { T *g = dst + obase + ooff_t;\n" : "    { T *g = st + base + off_t;\n");
+    if (pgp) o << "    { const u64 gy = obase + ooff_t;\n";
+    else o << (operm ? "    { T *g = dst + obase + ooff_t;\n" : "    { T *g = st + base + off_t;\n");
+    auto gst = [&](int it) {
+      return pgp ? "pst(gy + " + u64lit(PB(itoff[it])) + ")" : "g[" + u64lit(PB(itoff[it])) + "]";
+    };
     if (early) {
       std::vector<int> as;
       for (int it = 0; it < NE; it++) as.push_back((int)Sx(SO, (unsigned)(it * NT)));
       const auto ax = addr_group("sw_out", as, "      ");
       for (int it = 0; it < NE; it++) o << "      v[" << it << "] = " << ax[it] << ";\n";
       o << "      " << GS << "\n      " << next_issue << "\n";
-      for (int it = 0; it < NE; it++) o << "      g[" << u64lit(PB(itoff[it])) << "] = v[" << it << "];\n";
+      for (int it = 0; it < NE; it++) o << "      " << gst(it) << " = v[" << it << "];\n";
     } else {
       std::vector<int> as;
       for (int it = 0; it < NE; it++) as.push_back((int)Sx(SO, (unsigned)(it * NT)));
       const auto ax = addr_group("sw_out", as, "      ");
-      for (int it = 0; it < NE; it++) o << "      g[" << u64lit(PB(itoff[it])) << "] = " << ax[it] << ";\n";
+      for (int it = 0; it < NE; it++) o << "      " << gst(it) << " = " << ax[it] << ";\n";
     }
     o << "    }\n";
   }
@@ -1521,7 +1540,7 @@ bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->z
 // skip: non-active slots whose tiles with a 1 there are zero in and out (the
 // launch runs in place); those tiles are not visited at all
 cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
-                           uint64_t skip) {
+                           uint64_t skip, void *const *peers) {
   JitEntry *E = (JitEntry *)jit;
   const int NT = E->threads > 0 ? E->threads : 1 << (sl.K - sl.RB);
   if (E->attr_set < E->smem) {
@@ -1587,7 +1606,17 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
   uint64_t grid = (uint64_t)g_nsms * E->nt;
   if (grid > ntl) grid = ntl;
   if (sl.grid_cap > 0 && grid > (uint64_t)sl.grid_cap) grid = (uint64_t)sl.grid_cap;
-  void *args[] = {&st, &dst, &zmode, &nact, &ntl, &tmg};
+  struct PeerTab {
+    void *p[8];
+  } ptab = {};
+  if (sl.peer_gp > 0) {
+    if (!peers) return cudaErrorInvalidValue;
+    for (int b = 0; b < (1 << sl.peer_gp); b++) ptab.p[b] = peers[b];
+  }
+  void *args[8] = {&st, &dst, &zmode, &nact, &ntl};
+  int na = 5;
+  if (E->tma_rank) args[na++] = &tmg;
+  if (sl.peer_gp > 0) args[na++] = &ptab;
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
                           (size_t)E->smem, s);
 }

@@ -1344,7 +1344,34 @@ void build_plan(atlas_ctx *C, int s_max, double cf) {
         last.sl.out_perm_off = SW[k + 1].pre[sl][0].newpos_off;
         last.newpos_off = last.sl.out_perm_off;
         SW[k + 1].pre[sl].erase(SW[k + 1].pre[sl].begin());
+      } else if (C->opt.shm_fuse_pack && C->opt.shm_fuse_exchange && !C->opt.inplace_remap && !C->offload &&
+                 k + 1 < s && C->exch[k + 1].gp > 0 && C->exch[k + 1].gp <= 3 &&
+                 (SW[k + 1].pre[sl].empty() || SW[k + 1].pre[sl][0].type != L_PACK) && !C->prog[sl].empty() &&
+                 C->prog[sl].back().type == L_SHM && C->prog[sl].back().stage == k) {
+        // a remap without a pack: the identity "pack", so that the launch
+        // can carry the exchange below
+        Launch &last = C->prog[sl].back();
+        last.sl.out_perm_off = (int64_t)C->newpos.size();
+        last.newpos_off = last.sl.out_perm_off;
+        for (int b = 0; b < C->L; b++) C->newpos.push_back(b);
       }
+    }
+    // ... and the exchange itself: when every slot's last launch of the
+    // stage carries the fused pack, those launches store each packed block
+    // straight into the buffer of the rank it goes to (peer memory over
+    // NVLink, CUDA IPC; another slot's buffer in a virtual world), so no
+    // separate all-to-all runs (north_star (4); P:L1312 Shard).  All slots
+    // or none: a rank's stores land in its peers' buffers.
+    if (C->opt.shm_fuse_exchange && !C->offload && k + 1 < s && C->exch[k + 1].gp > 0 &&
+        C->exch[k + 1].gp <= 3) {
+      bool all = true;
+      for (int sl = 0; sl < C->nslots; sl++) {
+        const auto &P = C->prog[sl];
+        if (P.empty() || P.back().type != L_SHM || P.back().stage != k || P.back().sl.out_perm_off < 0)
+          all = false;
+      }
+      if (all)
+        for (int sl = 0; sl < C->nslots; sl++) C->prog[sl].back().sl.peer_gp = C->exch[k + 1].gp;
     }
   }
   C->planned = true;
@@ -1390,6 +1417,13 @@ std::string plan_json(const atlas_ctx *C) {
     o << "],\"flip_end\":[";
     for (int q = 0; q < C->n; q++) o << (q ? "," : "") << C->maps[k].flip_end[q];
     o << "],\"packed\":" << (k > 0 && C->exch[k].packed ? "true" : "false");
+    {
+      bool xf = false;  // the exchange rides on the previous stage's last launch
+      if (!C->prog.empty())
+        for (const Launch &ln : C->prog[0])
+          if (ln.stage == k - 1 && ln.type == L_SHM && ln.sl.peer_gp > 0) xf = true;
+      o << ",\"exchange_fused\":" << (xf ? "true" : "false");
+    }
     o << ",\"pack_fused\":";
     {
       int64_t off = -1;
@@ -1397,7 +1431,7 @@ std::string plan_json(const atlas_ctx *C) {
       if (!C->prog.empty())
         for (const Launch &ln : C->prog[0]) {
           if (ln.stage == k && ln.type == L_PACK) off = ln.newpos_off;
-          if (ln.stage == k - 1 && ln.type == L_SHM && ln.newpos_off >= 0) {
+          if (ln.stage == k - 1 && ln.type == L_SHM && ln.newpos_off >= 0 && C->exch[k].packed) {
             off = ln.newpos_off;
             fused = true;
           }

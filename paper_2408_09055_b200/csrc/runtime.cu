@@ -35,7 +35,7 @@ cudaError_t launch_swap_regions(int dtype, void *a, void *b, uint64_t n, cudaStr
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
 void shm_jit_prepare(atlas_ctx *C);
 cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
-                           uint64_t skip);
+                           uint64_t skip, void *const *peers);
 bool shm_jit_zero_ok(const void *jit);
 
 #define CK(x)                                                                              \
@@ -55,6 +55,8 @@ struct NcclApi {
   int (*send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
   int (*recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
   int (*commDestroy)(void *) = nullptr;
+  int (*allGather)(const void *, void *, size_t, int, void *, cudaStream_t) = nullptr;
+  int (*allReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
   const char *(*errStr)(int) = nullptr;
   void *commInitRank = nullptr;
 };
@@ -79,6 +81,9 @@ void nccl_load() {
   g_nccl.send = (int (*)(const void *, size_t, int, int, void *, cudaStream_t))dlsym(g_nccl.h, "ncclSend");
   g_nccl.recv = (int (*)(void *, size_t, int, int, void *, cudaStream_t))dlsym(g_nccl.h, "ncclRecv");
   g_nccl.commDestroy = (int (*)(void *))dlsym(g_nccl.h, "ncclCommDestroy");
+  g_nccl.allGather = (int (*)(const void *, void *, size_t, int, void *, cudaStream_t))dlsym(g_nccl.h, "ncclAllGather");
+  g_nccl.allReduce =
+      (int (*)(const void *, void *, size_t, int, int, void *, cudaStream_t))dlsym(g_nccl.h, "ncclAllReduce");
   g_nccl.errStr = (const char *(*)(int))dlsym(g_nccl.h, "ncclGetErrorString");
   g_nccl.commInitRank = dlsym(g_nccl.h, "ncclCommInitRank");
   if (!g_nccl.getUniqueId || !g_nccl.groupStart || !g_nccl.groupEnd || !g_nccl.send ||
@@ -94,6 +99,8 @@ void nccl_load() {
   } while (0)
 
 static const int kNcclUint8 = 1;  // ncclUint8 (nccl.h)
+static const int kNcclInt32 = 2;  // ncclInt32
+static const int kNcclSum = 0;    // ncclSum
 
 // ---------------------------------------------------------------- device
 static size_t amp_bytes(const atlas_ctx *C) { return C->dt == ATLAS_C128 ? 16 : 8; }
@@ -146,6 +153,41 @@ void ensure_device(atlas_ctx *C) {
     memcpy(u.internal, C->nccl_uid, 128);
     auto init = (int (*)(void **, int, Uid, int))g_nccl.commInitRank;
     NK(init(&C->nccl_comm, C->world, u, C->rank));
+  }
+  // fused exchange over peer memory: every rank opens every other rank's
+  // state and scratch shard (CUDA IPC handles allgathered over NCCL); the
+  // last shared-memory launch of a stage then stores each packed block
+  // straight into its destination rank's buffer over NVLink, and an
+  // allreduce of 4 bytes ends the exchange (library-owned buffers only)
+  if (C->world > 1 && C->nslots == 1 && C->nccl_comm && C->opt.shm_fuse_exchange && !C->opt.inplace_remap &&
+      !C->bound && !C->ipc_ready && g_nccl.allGather && g_nccl.allReduce) {
+    const int W = C->world;
+    cudaIpcMemHandle_t h[2];
+    CK(cudaIpcGetMemHandle(&h[0], C->d_state[0]));
+    CK(cudaIpcGetMemHandle(&h[1], C->d_scratch[0]));
+    void *d_h = nullptr;
+    CK(cudaMalloc(&d_h, (size_t)(W + 1) * sizeof h));
+    CK(cudaMemcpy(d_h, h, sizeof h, cudaMemcpyHostToDevice));
+    NK(g_nccl.allGather(d_h, (char *)d_h + sizeof h, sizeof h, kNcclUint8, C->nccl_comm, C->stream));
+    std::vector<cudaIpcMemHandle_t> all(2 * (size_t)W);
+    CK(cudaMemcpyAsync(all.data(), (char *)d_h + sizeof h, (size_t)W * sizeof h, cudaMemcpyDeviceToHost,
+                       C->stream));
+    CK(cudaStreamSynchronize(C->stream));
+    cudaFree(d_h);
+    C->ipc_state.assign(W, nullptr);
+    C->ipc_scratch.assign(W, nullptr);
+    for (int r = 0; r < W; r++) {
+      if (r == C->rank) {
+        C->ipc_state[r] = C->d_state[0];
+        C->ipc_scratch[r] = C->d_scratch[0];
+        continue;
+      }
+      CK(cudaIpcOpenMemHandle(&C->ipc_state[r], all[2 * r], cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&C->ipc_scratch[r], all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+    }
+    CK(cudaMalloc(&C->d_bar, 4));
+    CK(cudaMemset(C->d_bar, 0, 4));
+    C->ipc_ready = true;
   }
   if (C->world > 1 && C->opt.inplace_remap && C->nslots == 1 && !C->d_stage) {
     // receive staging of the in-place exchange: one chunk
@@ -235,6 +277,33 @@ std::vector<Xfer> exchange_schedule(const atlas_ctx *C, int k, int r) {
     v.push_back(Xfer{p, XFER_RECV, 0, (uint64_t)bt * blk, blk});
   }
   return v;
+}
+
+// Fused exchange (option shm_fuse_exchange): the last shared-memory launch
+// of stage k-1 stores block b of its packed output (the block the schedule
+// sends to rank rd) straight at the offset rank rd receives it at, in rd's
+// idle buffer -- a peer's memory over NVLink (CUDA IPC), or another slot's
+// buffer in a virtual world.  remote = false: every block to this slot's
+// own other buffer (a plain fused pack; the exchange then runs as usual).
+static void *rank_other_buf(atlas_ctx *C, int rank) {
+  if (C->nslots > 1) return other_buf(C, rank);
+  if (rank == C->rank) return other_buf(C, 0);
+  return C->cur[0] ? C->ipc_state[rank] : C->ipc_scratch[rank];
+}
+static bool peer_exchange_ok(const atlas_ctx *C) { return C->nslots > 1 || C->ipc_ready; }
+static void fill_peers(atlas_ctx *C, int k, int s, void **peers, bool remote) {
+  const int r = slot_rank(C, s);
+  const uint64_t blk = (uint64_t)amp_bytes(C) << (C->L - C->exch[k].gp);
+  for (const Xfer &x : exchange_schedule(C, k, r)) {
+    if (x.kind == XFER_RECV) continue;
+    const int b = (int)(x.src_off / blk);
+    if (!remote) {
+      peers[b] = (char *)other_buf(C, s) + x.src_off;
+      continue;
+    }
+    const uint64_t doff = x.kind == XFER_LOCAL ? x.dst_off : recv_offset(C, k, r, x.peer);
+    peers[b] = (char *)rank_other_buf(C, x.peer) + doff;
+  }
 }
 
 // Exchange of stage k (after the optional pack) for all local slots.
@@ -445,7 +514,7 @@ static void run_offload(atlas_ctx *C) {
             const bool operm = sl.out_perm_off >= 0;
             void *dst = operm ? C->d_work[w ^ 1] : st;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z, 0));
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z, 0, nullptr));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                             (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
@@ -581,10 +650,26 @@ void run(atlas_ctx *C) {
       }
   const int S = C->sp.s;
   std::vector<size_t> pc(C->nslots, 0);
+  std::vector<char> fused_x(S + 1, 0);  // remap k's exchange done by the launches (fused)
   const double2 *mats = (const double2 *)C->d_mats;
   for (int k = 0; k < S; k++) {
-    // remap: pack (per slot), then exchange (all slots together)
-    if (k > 0 && C->exch[k].gp > 0) {
+    if (k > 0 && C->exch[k].gp > 0 && fused_x[k]) {
+      // every slot's last launch of stage k-1 stored its blocks at their
+      // destinations: the data is in every rank's other buffer; ranks that
+      // are separate processes agree on it with a 4-byte allreduce, which
+      // completes only after every rank's stores (stream order)
+      for (int s = 0; s < C->nslots; s++) {
+        auto &P = C->prog[s];
+        while (pc[s] < P.size() && P[pc[s]].stage == k && P[pc[s]].type == L_EXCHANGE) pc[s]++;
+      }
+      mark(L_EXCHANGE, 0);
+      if (C->nslots == 1 && C->world > 1)
+        NK(g_nccl.allReduce(C->d_bar, C->d_bar, 1, kNcclInt32, kNcclSum, C->nccl_comm, C->stream));
+      mark_end();
+      for (int s = 0; s < C->nslots; s++) C->cur[s] ^= 1;
+      std::fill(zq.begin(), zq.end(), 0);
+      std::fill(zall.begin(), zall.end(), false);
+    } else if (k > 0 && C->exch[k].gp > 0) {
       for (int s = 0; s < C->nslots; s++) {
         auto &P = C->prog[s];
         while (pc[s] < P.size() && P[pc[s]].stage == k && P[pc[s]].type == L_PACK) {
@@ -643,8 +728,13 @@ void run(atlas_ctx *C) {
             // a fused remap pack writes the permuted output to the other buffer
             const bool operm = sl.out_perm_off >= 0;
             void *dst = operm ? other_buf(C, s) : st;
+            // ... and a fused exchange to the destination ranks' buffers
+            const bool pex = operm && sl.peer_gp > 0 && ln.jit && peer_exchange_ok(C);
+            void *peers[8] = {nullptr};
+            if (operm && sl.peer_gp > 0 && ln.jit) fill_peers(C, k + 1, s, peers, pex);
+            if (pex) fused_x[k + 1] = 1;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm, skip));
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm, skip, peers));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                             (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
@@ -653,7 +743,7 @@ void run(atlas_ctx *C) {
                 CK(launch_permute(dt, st, dst, C->L, &C->newpos[sl.out_perm_off],
                                   (const int *)C->d_newpos + sl.out_perm_off, C->stream));
             }
-            if (operm) C->cur[s] ^= 1;
+            if (operm && !pex) C->cur[s] ^= 1;
             break;
           }
           case L_SCALE: CK(launch_scale(dt, st, C->L, ln.sre, ln.sim, C->stream)); break;
@@ -831,6 +921,14 @@ void destroy(atlas_ctx *C) {
     for (void *p : {C->d_coef, C->d_ops, C->d_phases, C->d_mats, C->d_newpos, C->d_ents, C->d_terms, C->d_stage})
       if (p) cudaFree(p);
     for (auto e : C->ev) cudaEventDestroy(e);
+    if (C->ipc_ready) {
+      for (int r = 0; r < (int)C->ipc_state.size(); r++)
+        if (r != C->rank) {
+          cudaIpcCloseMemHandle(C->ipc_state[r]);
+          cudaIpcCloseMemHandle(C->ipc_scratch[r]);
+        }
+      if (C->d_bar) cudaFree(C->d_bar);
+    }
     if (C->own_stream) cudaStreamDestroy(C->stream);
     if (C->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(C->nccl_comm);
   }

@@ -134,7 +134,8 @@ def test_qsvm_n28_mirror_repeated():
             assert np.abs(rest).max() <= 1e-10
 
 
-@pytest.mark.parametrize("opt", [{"shm_fuse_pack": 0}, {"shm_jit": 0}, {"shm_grid": 2}])
+@pytest.mark.parametrize("opt", [{"shm_fuse_pack": 0}, {"shm_jit": 0}, {"shm_grid": 2},
+                                 {"shm_fuse_exchange": 0}, {"zero_skip": 0}])
 @pytest.mark.parametrize("W", [2, 8])
 def test_fused_pack_variants(W, opt):
     """The remap pack fused into the previous stage's last shared-memory
@@ -156,6 +157,9 @@ def test_fused_pack_present():
         pj = s.plan_json()
     packed = [st for st in pj["stages"] if st["packed"]]
     assert packed and all(st["pack_fused"] for st in packed)
+    # the exchange rides on the same launches (stores into the destination
+    # ranks' buffers): no separate all-to-all for those remaps
+    assert all(st["exchange_fused"] for st in packed)
 
 
 @pytest.mark.parametrize("W", [2, 4, 8])
