@@ -101,6 +101,7 @@ void nccl_load() {
 static const int kNcclUint8 = 1;  // ncclUint8 (nccl.h)
 static const int kNcclInt32 = 2;  // ncclInt32
 static const int kNcclSum = 0;    // ncclSum
+static const int kNcclMin = 3;    // ncclMin
 
 // ---------------------------------------------------------------- device
 static size_t amp_bytes(const atlas_ctx *C) { return C->dt == ATLAS_C128 ? 16 : 8; }
@@ -162,32 +163,56 @@ void ensure_device(atlas_ctx *C) {
   if (C->world > 1 && C->nslots == 1 && C->nccl_comm && C->opt.shm_fuse_exchange && !C->opt.inplace_remap &&
       !C->bound && !C->ipc_ready && g_nccl.allGather && g_nccl.allReduce) {
     const int W = C->world;
+    // every rank must agree on using peer memory (a rank that could not
+    // open a peer's buffers makes all of them keep the NCCL exchange)
+    int ok = 1;
     cudaIpcMemHandle_t h[2];
-    CK(cudaIpcGetMemHandle(&h[0], C->d_state[0]));
-    CK(cudaIpcGetMemHandle(&h[1], C->d_scratch[0]));
+    if (cudaIpcGetMemHandle(&h[0], C->d_state[0]) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h[1], C->d_scratch[0]) != cudaSuccess) {
+      ok = 0;
+      memset(h, 0, sizeof h);
+    }
     void *d_h = nullptr;
-    CK(cudaMalloc(&d_h, (size_t)(W + 1) * sizeof h));
+    CK(cudaMalloc(&d_h, (size_t)(W + 1) * sizeof h + 8));
     CK(cudaMemcpy(d_h, h, sizeof h, cudaMemcpyHostToDevice));
     NK(g_nccl.allGather(d_h, (char *)d_h + sizeof h, sizeof h, kNcclUint8, C->nccl_comm, C->stream));
     std::vector<cudaIpcMemHandle_t> all(2 * (size_t)W);
     CK(cudaMemcpyAsync(all.data(), (char *)d_h + sizeof h, (size_t)W * sizeof h, cudaMemcpyDeviceToHost,
                        C->stream));
     CK(cudaStreamSynchronize(C->stream));
-    cudaFree(d_h);
     C->ipc_state.assign(W, nullptr);
     C->ipc_scratch.assign(W, nullptr);
-    for (int r = 0; r < W; r++) {
+    for (int r = 0; r < W && ok; r++) {
       if (r == C->rank) {
         C->ipc_state[r] = C->d_state[0];
         C->ipc_scratch[r] = C->d_scratch[0];
         continue;
       }
-      CK(cudaIpcOpenMemHandle(&C->ipc_state[r], all[2 * r], cudaIpcMemLazyEnablePeerAccess));
-      CK(cudaIpcOpenMemHandle(&C->ipc_scratch[r], all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+      if (cudaIpcOpenMemHandle(&C->ipc_state[r], all[2 * r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+          cudaIpcOpenMemHandle(&C->ipc_scratch[r], all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess) !=
+              cudaSuccess)
+        ok = 0;
     }
-    CK(cudaMalloc(&C->d_bar, 4));
-    CK(cudaMemset(C->d_bar, 0, 4));
-    C->ipc_ready = true;
+    cudaGetLastError();  // a failed open is handled by the agreement below
+    int *d_ok = (int *)((char *)d_h + (size_t)(W + 1) * sizeof h);
+    CK(cudaMemcpy(d_ok, &ok, 4, cudaMemcpyHostToDevice));
+    NK(g_nccl.allReduce(d_ok, d_ok, 1, kNcclInt32, kNcclMin, C->nccl_comm, C->stream));
+    CK(cudaMemcpyAsync(&ok, d_ok, 4, cudaMemcpyDeviceToHost, C->stream));
+    CK(cudaStreamSynchronize(C->stream));
+    cudaFree(d_h);
+    if (ok) {
+      CK(cudaMalloc(&C->d_bar, 4));
+      CK(cudaMemset(C->d_bar, 0, 4));
+      C->ipc_ready = true;
+    } else {
+      for (int r = 0; r < W; r++)
+        if (r != C->rank) {
+          if (C->ipc_state[r]) cudaIpcCloseMemHandle(C->ipc_state[r]);
+          if (C->ipc_scratch[r]) cudaIpcCloseMemHandle(C->ipc_scratch[r]);
+        }
+      C->ipc_state.clear();
+      C->ipc_scratch.clear();
+    }
   }
   if (C->world > 1 && C->opt.inplace_remap && C->nslots == 1 && !C->d_stage) {
     // receive staging of the in-place exchange: one chunk
