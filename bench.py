@@ -242,6 +242,14 @@ def load_traffic():
         return {}
 
 
+def bench_config(fam, n, m, world, fp64=True):
+    """The workload this line measures -- identical for both arms (the
+    implementation's own details go to the line's 'details')."""
+    amp = 16 if fp64 else 8
+    return {"workload": f"{fam}_n{n}_{'fp64' if fp64 else 'fp32'}", "n": n, "gates": m,
+            "l2": "state (%.0f GiB/GPU) >> L2; no flush needed" % (amp * 2 ** (n - int(math.log2(world))) / 2 ** 30)}
+
+
 # ------------------------------------------------------------- reference
 def run_reference(args):
     """The tier's reference arm: the oracle as it stands (OpenMP build, every
@@ -270,9 +278,9 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{fam}_n{n}_fp64", "n": n, "gates": len(circ.gates),
-                   "sample_gates_per_step": per},
+        "config": bench_config(fam, n, len(circ.gates), args.gpus),
         "cpu_baseline": {"value": value, "unit": "amp-updates/s", "cores": nthr, "kind": "oracle",
+                         "sample_gates_per_step": per,
                          "sample": f"first {per} of {len(circ.gates)} gates of {fam} n={n} "
                                    f"(complex128, gate-at-a-time C oracle, OpenMP over {nthr} "
                                    f"host threads) per step", "host": host_info()},
@@ -509,10 +517,10 @@ def run_atlas(args):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"{fam}_n{n}_{'fp64' if dtype == A.C128 else 'fp32'}",
-                   "n": n, "gates": m, "L": stats["L"], "G": stats["G"],
-                   "parallelism": f"state sharded over {world} GPU(s), NCCL remaps",
-                   "l2": "state (%.0f GiB/GPU) >> L2; no flush needed" % ((16 if dtype == A.C128 else 8) * 2 ** (n - int(math.log2(world))) / 2 ** 30),
+        "config": bench_config(fam, n, m, world, dtype == A.C128),
+        "details": {"L": stats["L"], "G": stats["G"],
+                   "parallelism": f"state sharded over {world} GPU(s); remaps fused into the last "
+                                  f"shared-memory launch of a stage (peer stores) or NCCL send/recv",
                    "plan": pj, "kernel_ms_per_step": kinds_ms,
                    "remap_ms_per_step": round(remap_ms, 4),
                    "kernels_ms_per_step_total": round(step_kernel_ms, 4),

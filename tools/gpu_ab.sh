@@ -14,7 +14,7 @@ for opt in ${OPTS:--}; do
   python -c "
 import json
 d=json.loads(open('$O/${T}_q.json').read().strip().splitlines()[-1])
-c=d['config']; r=d['roofline']
+c=d.get('details', d['config']); r=d['roofline']
 print('$w $opt', d['ms_per_step'], '%.3g'%d['value'], c['plan']['kernels'], r['frac'], r['avg_launch_ms'], d['clocks']['sm_mhz'], d['clocks']['reasons'])
 " || tail -3 $O/${T}_q.err
 done; done

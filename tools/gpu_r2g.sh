@@ -10,7 +10,7 @@ for w in qft_n28 ghz_n28 graphstate_n28 qsvm_n28 wstate_n28 ising_n28; do
   python -c "
 import json
 d=json.loads(open('$O/r2g_$w.json').read().strip().splitlines()[-1])
-c=d['config']; r=d['roofline']
+c=d.get('details', d['config']); r=d['roofline']
 print('$w', d['ms_per_step'], '%.3g'%d['value'], c['plan']['kernels'], r['frac'], r['avg_launch_ms'], d['clocks']['sm_mhz'])
 " || tail -3 $O/r2g_$w.err
 done
@@ -19,7 +19,7 @@ for w in su2random_n28 qft_n28; do
   python -c "
 import json
 d=json.loads(open('$O/r2g_${w}_f32.json').read().strip().splitlines()[-1])
-c=d['config']; r=d['roofline']
+c=d.get('details', d['config']); r=d['roofline']
 print('$w f32', d['ms_per_step'], '%.3g'%d['value'], c['plan']['kernels'], r['frac'], r['avg_launch_ms'], d['clocks']['sm_mhz'])
 " || tail -3 $O/r2g_${w}_f32.err
 done
@@ -28,7 +28,7 @@ for w in su2random_n33 qft_n33; do
   python -c "
 import json
 d=json.loads(open('$O/r2g_$w.json').read().strip().splitlines()[-1])
-c=d['config']; r=d['roofline']
+c=d.get('details', d['config']); r=d['roofline']
 print('$w', d['ms_per_step'], '%.3g'%d['value'], c['plan']['kernels'], r['frac'], r['avg_launch_ms'], d['clocks']['sm_mhz'])
 " || tail -3 $O/r2g_$w.err
 done
