@@ -231,6 +231,11 @@ const char *atlas_last_error(void);
  *                    n = 28 2.267 vs 2.273 ms) and some n = 28 runs stall
  *                    on a tile that never completes (the kernel traps after
  *                    ~10 s), so off by default [0]
+ *   "shm_fold_perm"  plan-specialised kernels: a leading register phase that
+ *                    carries only a folded permutation (X/CX/SWAP) is not
+ *                    run; the tile load writes every element straight to its
+ *                    permuted position (one shared-memory round trip fewer)
+ *                    [1]
  *   "shm_addr_split" plan-specialised kernels address a phase's shared-memory
  *                    elements as (x ^ low) + high: one pointer per distinct
  *                    low (bank-bit) part, immediate offsets for the rest [1]

@@ -277,6 +277,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "zero_skip") { o.zero_skip = (int)v; replan = false; }
     else if (k == "shm_tma") { o.shm_tma = (int)v; C->jit_ready = false; replan = false; }
+    else if (k == "shm_fold_perm") { o.shm_fold_perm = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_addr_split") { o.shm_addr_split = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_lit_smem") { o.shm_lit_smem = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_fuse_exchange") o.shm_fuse_exchange = (int)v;

@@ -87,6 +87,7 @@ struct Options {
   int shm_grid = 0;          // > 0: cap every SHM launch at this many CTAs (tests: many tiles per CTA at small n)
   int shm_const_pool = 0;    // JIT fp64: coefficients in a __constant__ table (c[] operands, no UMOV)
   int shm_tma = 0;           // JIT fp64 pipe: tile loads as one TMA tensor copy (experimental, off: see DESIGN 5e)
+  int shm_fold_perm = 1;     // JIT: a leading permutation-only phase folded into the tile load
   int shm_addr_split = 1;    // JIT: shared-memory addresses as (x ^ low) + high (immediate offsets)
   int shm_lit_smem = 0;      // JIT fp64: diagonal-run element factors read from a shared-memory table
   int zero_skip = 1;         // runs from |0...0>: tiles provably zero in and out are not visited

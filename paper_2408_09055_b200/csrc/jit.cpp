@@ -462,6 +462,15 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     }
   const int lastp = sl.nphase - 1;
   const bool ld_ = sl.last_direct != 0;
+  // fold0: a leading phase with no op but its folded permutation (a CX
+  // block whose dense gates come later) only moves the tile through shared
+  // memory once more; its permuted store is folded into the tile load
+  // instead -- every cp.async writes its element straight to the permuted
+  // (and re-swizzled) position -- and the phase is not emitted (option
+  // shm_fold_perm; cp.async loads only, not when the phase's gather feeds a
+  // direct HBM store)
+  const bool fold0 = C->opt.shm_fold_perm && nbuf == 1 && !tma && sl.nphase >= 1 && ph[0].permuted &&
+                     ph[0].op_begin == ph[0].op_end && !(ld_ && lastp == 0);
   std::vector<int> rmask(sl.nphase), gsw(sl.nphase, 0), ssw(sl.nphase, 0);
   std::vector<unsigned> qln(sl.nphase, 0xffff);
   for (int p = 0; p < sl.nphase; p++) {
@@ -508,7 +517,41 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     return q;
   };
   std::mt19937 rng(12345u);  // deterministic: identical on every rank
-  for (int p = 0; p < sl.nphase; p++) {
+  bool fold_ok = false;
+  if (fold0) {
+    // the load writes with lanes = tile bits 0..W-1 (8 / 16 consecutive
+    // threads): find a layout under which those lanes' permuted images hit
+    // W bank groups and the next phase can gather conflict-free
+    std::vector<int> ll;
+    for (int b = 0; b < W; b++) ll.push_back(b);
+    for (int trial = 0; trial < 400 && !fold_ok; trial++) {
+      Swz T(K, 0);
+      if (trial == 0) T = swzs[0];
+      else
+        for (int b = W; b < K; b++) T[b] = rng() & WM;
+      if (store_rank(0, ll, T) != W) continue;
+      bool next_ok = sl.nphase == 1;
+      if (!next_ok)
+        for (auto &s2 : subsets(1))
+          if (gather_rank(s2, T) == W) {
+            next_ok = true;
+            break;
+          }
+      if (!next_ok) continue;
+      int ti = -1;
+      for (size_t i = 0; i < swzs.size(); i++)
+        if (swzs[i] == T) ti = (int)i;
+      if (ti < 0) {
+        ti = (int)swzs.size();
+        swzs.push_back(T);
+      }
+      qln[0] = enc(ll);
+      ssw[0] = ti;
+      if (sl.nphase > 1) gsw[1] = ti;
+      fold_ok = true;
+    }
+  }
+  for (int p = fold_ok ? 1 : 0; p < sl.nphase; p++) {
     const Swz G = swzs[gsw[p]];
     const auto subs = subsets(p);
     if (subs.empty()) continue;
@@ -716,7 +759,8 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // zmode (early pipeline only): 1 = the input is all zeros, 2 = the input
   // is |0...0> on this rank (atlas_run's initial state): the first tile
   // load is synthesised in registers and nothing is read from HBM
-  o << "#define ZERO_OK " << (nbuf == 1 ? 1 : 0) << "\n";
+  o << "#define ZERO_OK " << (nbuf == 1 && !fold_ok ? 1 : 0) << "\n";
+  if (fold_ok) o << "// phase 0 (a permutation only) folded into the tile load\n";
   o << "__device__ __forceinline__ u64 pdep64(u64 v, u64 mask) { u64 r = 0; while (mask) { u64 lo = "
        "mask & (~mask + 1); if (v & 1) r |= lo; v >>= 1; mask ^= lo; } return r; }\n";
   o << "#define BLOCK_THREADS " << BT << "\n";
@@ -835,8 +879,17 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "\n  u64 ooff_t = 0;";
     for (int i = 0; i < K - RB; i++) o << " if ((tid >> " << i << ") & 1) ooff_t |= " << u64lit(PB(1ull << sl.act[i])) << ";";
   }
+  // load destination of this thread's elements: the load layout, or (fold0)
+  // the permuted, re-swizzled position phase 0 would have stored them at
+  auto ldimg = [&](unsigned j) {
+    if (!fold_ok) return Sx(swzs[0], j);
+    unsigned r = 0;
+    for (int b = 0; b < K; b++)
+      if ((j >> b) & 1) r ^= simg[0][b];
+    return r;
+  };
   o << "\n  int sw_tid = 0;";
-  for (int t = 0; t < K - RB; t++) o << " if ((tid >> " << t << ") & 1) sw_tid ^= " << Sx(swzs[0], 1u << t) << ";";
+  for (int t = 0; t < K - RB; t++) o << " if ((tid >> " << t << ") & 1) sw_tid ^= " << ldimg(1u << t) << ";";
   o << "\n";
   // copy-out reads the layout of the last boundary
   const Swz &SO = swzs[ssw[lastp]];
@@ -866,9 +919,19 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     itoff[it] = x;
   }
   o << "  auto issue_load = [&](int bsel, " << (pipe ? "int msel, " : "") << "u64 base) {\n    const T *g = st + base + off_t;\n";
+  if (fold_ok) {
+    // phase 0's constant and tile-dependent offsets (the folded map's
+    // translation and its CX controlled by non-active qubits)
+    o << "    int swl = sw_tid ^ " << Sx(swzs[ssw[0]], Ac0[0]) << ";\n";
+    for (int i = ph[0].term_begin; i < ph[0].term_end; i++)
+      o << "    if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
+        << ") swl ^= " << Sx(swzs[ssw[0]], Sx(GL, terms[i].vec_swz)) << ";\n";
+  } else {
+    o << "    const int swl = sw_tid;\n";
+  }
   for (int it = 0; it < NE; it++) {
-    o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (sw_tid ^ "
-      << Sx(swzs[0], (unsigned)(it * NT)) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
+    o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (swl ^ "
+      << ldimg((unsigned)(it * NT)) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
     if (!f32) o << "asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
     else o << "asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
   }
@@ -1063,7 +1126,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "    T v[" << NE << "];\n";
   double pend = 1.0;  // deferred uniform scalar (sign blocks)
   const bool defer_scalar = C->opt.shm_defer_scalar != 0;
-  for (int p = 0; p < sl.nphase; p++) {
+  for (int p = fold_ok ? 1 : 0; p < sl.nphase; p++) {
     const ShmPhase &P = ph[p];
     int sr[4] = {0, 0, 0, 0};
     for (int i = 0; i < RB; i++) sr[i] = (int)Sx(swzs[gsw[p]], 1u << P.rbit[i]);

@@ -87,7 +87,8 @@ def test_bench_config_mirror_full_state(fam):
 
 @pytest.mark.parametrize("opt", [{}, {"shm_pipe": 0}, {"shm_pipe": 0, "shm_ctas": 3},
                                  {"shm_direct_store": 0}, {"shm_tfac_min": 0},
-                                 {"zero_skip": 0}, {"shm_addr_split": 0}, {"shm_lit_smem": 1}])
+                                 {"zero_skip": 0}, {"shm_addr_split": 0}, {"shm_lit_smem": 1},
+                                 {"shm_fold_perm": 0}])
 @pytest.mark.parametrize("fam", ["su2random", "qsvm", "ising", "qft", "random"])
 def test_grid_capped_many_tiles(fam, opt):
     """A grid of 3 CTAs at n = 18 (64 tiles): each pipe group runs ~10 tiles

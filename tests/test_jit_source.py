@@ -101,3 +101,18 @@ def test_jit_pipe_variant_compiles(fam, pipe, tmp_path):
         m = re.search(r"__launch_bounds__\((\d+), (\d+)\)", src)
         regs, spill = ptxas(src, tmp_path, f"p{i}")
         assert regs * int(m.group(1)) * int(m.group(2)) <= 65536 and spill == 0
+
+
+def test_fold_leading_permutation_phase():
+    """A leading phase that only carries a folded permutation (su2random's
+    CX block before the next U3 layer) is folded into the tile load: the
+    kernel says so, cannot synthesise |0...0> (ZERO_OK 0) and emits one
+    phase fewer; with shm_fold_perm = 0 the phase is emitted."""
+    c = C.su2random(28)
+    on = sources(c)
+    off = sources(c, shm_fold_perm=0)
+    folded = [i for i, src in enumerate(on) if "folded into the tile load" in src]
+    assert folded, "no kernel folded its leading permutation phase"
+    for i in folded:
+        assert "#define ZERO_OK 0" in on[i]
+        assert on[i].count("{ // phase ") == off[i].count("{ // phase ") - 1
