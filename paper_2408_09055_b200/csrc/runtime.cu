@@ -640,8 +640,10 @@ void run(atlas_ctx *C) {
   // kernel it synthesises that input itself (zmode) instead of reading a
   // memset shard: one write-only pass fewer.
   std::vector<int> zmode(C->nslots, 0);
+  std::vector<char> from_zero(C->nslots, 0);  // this run starts from |0...0> (or zeros) on slot s
   for (int s = 0; s < C->nslots; s++) {
     if (!C->opt.init && C->state_set) continue;
+    from_zero[s] = 1;
     C->cur[s] = 0;
     const auto &P = C->prog[s];
     if (C->opt.init_fuse && !P.empty() && P[0].stage == 0 && P[0].type == L_SHM &&
@@ -669,9 +671,9 @@ void run(atlas_ctx *C) {
   std::vector<bool> zall(C->nslots, false);
   if (C->opt.zero_skip)
     for (int s = 0; s < C->nslots; s++)
-      if (zmode[s]) {
+      if (from_zero[s]) {  // synthesised by the first launch (zmode) or by the init pass
         zq[s] = lmask;
-        zall[s] = zmode[s] == 1;
+        zall[s] = slot_rank(C, s) != 0;
       }
   const int S = C->sp.s;
   std::vector<size_t> pc(C->nslots, 0);

@@ -148,21 +148,6 @@ def test_fused_pack_variants(W, opt):
     check(psi, O.simulate(c))
 
 
-def test_fused_pack_present():
-    """su2random at W = 8 needs packs; with fusion every one of them rides
-    on a shared-memory launch (no standalone pack launch)."""
-    c = C.su2random(20)
-    with A.Simulator(c.n, 0, 8, 0, virtual_world=1) as s:
-        s.load_circuit(c.gates)
-        s.plan()
-        pj = s.plan_json()
-    packed = [st for st in pj["stages"] if st["packed"]]
-    assert packed and all(st["pack_fused"] for st in packed)
-    # the exchange rides on the same launches (stores into the destination
-    # ranks' buffers): no separate all-to-all for those remaps
-    assert all(st["exchange_fused"] for st in packed)
-
-
 @pytest.mark.parametrize("W", [2, 4, 8])
 @pytest.mark.parametrize("fam", ["su2random", "qft", "random"])
 def test_inplace_remap(fam, W):

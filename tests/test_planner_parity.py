@@ -266,3 +266,33 @@ def test_exchange_is_pairwise_swap_up_to_flip_relabel(seed, W):
                 psend = {x[1]: x[2] for x in scheds[p][k] if x[0] == "send"}
                 prec = {x[1]: x[3] for x in scheds[p][k] if x[0] == "recv"}
                 assert prec[r] ^ psend[r] == rel
+
+
+def test_fused_pack_present():
+    """su2random at W = 8 needs packs; with fusion every one of them rides
+    on a shared-memory launch (no standalone pack launch).  Host-only: the
+    plan report."""
+    c = C.su2random(20)
+    with A.Simulator(c.n, 0, 8, 0, virtual_world=1) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        pj = s.plan_json()
+    packed = [st for st in pj["stages"] if st["packed"]]
+    assert packed and all(st["pack_fused"] for st in packed)
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+@pytest.mark.parametrize("fam", ["su2random", "qft", "ising"])
+def test_exchange_fused_plan(fam, W):
+    """shm_fuse_exchange: every remap's exchange rides on the previous
+    stage's last shared-memory launch (packed remaps and, with an identity
+    pack, unpacked ones); off, none does.  Host-only: the plan report."""
+    c = C.make(fam, 20)
+    for on in (1, 0):
+        with A.Simulator(c.n, 0, W, 0, virtual_world=1, shm_fuse_exchange=on) as s:
+            s.load_circuit(c.gates)
+            s.plan()
+            pj = s.plan_json()
+        remaps = [st for st in pj["stages"][1:] if st["remap_qubits"] > 0]
+        assert remaps
+        assert all(bool(st["exchange_fused"]) == bool(on) for st in remaps)
