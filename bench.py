@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--kernelizer", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-compare", action="store_true",
+                   help="skip re-timing the steps without zero-support tracking (profiling runs)")
     p.add_argument("--opt", action="append", default=[], help="extra library option key=int")
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                    help="weak: n = workload n + log2 N (28 local qubits per GPU, the "
@@ -366,7 +368,7 @@ def run_atlas(args):
     # the support the circuit has reached from |0...0>), so the effect of
     # that exact optimisation on the headline is visible
     no_skip = None
-    if extra.get("zero_skip", 1):
+    if extra.get("zero_skip", 1) and not args.no_compare:
         sim.set_option("zero_skip", 0)
         for _ in range(2):
             sim.run()
