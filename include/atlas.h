@@ -216,6 +216,13 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
+ *   "async"          1 = atlas_run, and atlas_set_state / atlas_get_state
+ *                    when the layout is the identity (contiguous copies),
+ *                    return once the work is enqueued on the context's
+ *                    stream (atlas_set_stream) without synchronising it; the
+ *                    caller synchronises that stream before it touches the
+ *                    host buffers or the result (lets two contexts overlap
+ *                    host<->device copies with compute) [0]
  *   "zero_skip"      1 = a run that starts from |0...0> tracks the local
  *                    slots no launch has made active yet (they are still 0):
  *                    an in-place plan-specialised shared-memory launch does

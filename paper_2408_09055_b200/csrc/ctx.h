@@ -90,6 +90,7 @@ struct Options {
   int shm_fold_perm = 1;     // JIT: a leading permutation-only phase folded into the tile load
   int shm_addr_split = 1;    // JIT: shared-memory addresses as (x ^ low) + high (immediate offsets)
   int shm_lit_smem = 0;      // JIT fp64: diagonal-run element factors read from a shared-memory table
+  int async = 0;             // run / set_state / get_state (contiguous layouts) return without a stream sync
   int zero_skip = 1;         // runs from |0...0>: tiles provably zero in and out are not visited
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter
   long long dp_budget = 250000;

@@ -780,7 +780,7 @@ void run(atlas_ctx *C) {
       }
     }
   }
-  CK(cudaStreamSynchronize(C->stream));
+  if (!C->opt.async || timing) CK(cudaStreamSynchronize(C->stream));  // async: the caller syncs its stream
   if (timing) {
     for (size_t i = 0; i < rec.size(); i++) {
       float ms = 0;
@@ -841,7 +841,7 @@ void get_state(atlas_ctx *C, void *host, uint64_t first, uint64_t count) {
                            C->stream));
       x += len;
     }
-    CK(cudaStreamSynchronize(C->stream));
+    if (!C->opt.async) CK(cudaStreamSynchronize(C->stream));  // async: the caller syncs its stream
     return;
   }
   // general layout, few amplitudes (sampled checks at capacity): one small
@@ -902,7 +902,7 @@ void set_state(atlas_ctx *C, const void *host, uint64_t first, uint64_t count) {
                            kind, C->stream));
       x += len;
     }
-    CK(cudaStreamSynchronize(C->stream));
+    if (!C->opt.async) CK(cudaStreamSynchronize(C->stream));  // async: the caller syncs its stream
     C->state_set = true;
     return;
   }
