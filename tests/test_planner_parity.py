@@ -296,3 +296,19 @@ def test_exchange_fused_plan(fam, W):
         remaps = [st for st in pj["stages"][1:] if st["remap_qubits"] > 0]
         assert remaps
         assert all(bool(st["exchange_fused"]) == bool(on) for st in remaps)
+
+
+@pytest.mark.parametrize("key", ["async", "zero_skip", "init", "timing", "shm_addr_split", "shm_fold_perm",
+                                 "shm_lit_smem", "shm_tma"])
+def test_runtime_options_keep_the_plan(key):
+    """Options that only change how a plan runs (not the plan) can be set
+    between atlas_plan and atlas_run: the plan stays valid (host-only)."""
+    c = C.su2random(14)
+    with A.Simulator(c.n, 0, 1, 0) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        before = s.plan_json()
+        s.set_option(key, 1)
+        s.set_option(key, 0)
+        assert s.plan_json() == before
+        assert s.jit_source(0)
