@@ -275,6 +275,7 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_pipe") { o.shm_pipe = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_ctas") { need(v == 2 || v == 3, ATLAS_E_INVALID, "shm_ctas is 2 or 3"); o.shm_ctas = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
+    else if (k == "shm_autotune") { o.shm_autotune = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "async") { o.async = (int)v; replan = false; }
     else if (k == "zero_skip") { o.zero_skip = (int)v; replan = false; }
     else if (k == "shm_tma") { o.shm_tma = (int)v; C->jit_ready = false; replan = false; }

@@ -22,6 +22,10 @@ struct Launch {
   double sre = 1, sim = 0;   // L_SCALE
   int64_t bytes = 0;         // algorithmic HBM bytes
   void *jit = nullptr;       // L_SHM: plan-specialised kernel (jit.cpp), or null
+  // autotuning (option shm_autotune): the other pipeline variant of the same
+  // launch and the device time each variant took in the tuning runs
+  void *jit_alt = nullptr;
+  float tune_ms[2] = {-1.f, -1.f};
 };
 
 // Exchange of one remap (stage boundary k-1 -> k): swap the g' top local
@@ -90,6 +94,7 @@ struct Options {
   int shm_fold_perm = 1;     // JIT: a leading permutation-only phase folded into the tile load
   int shm_addr_split = 1;    // JIT: shared-memory addresses as (x ^ low) + high (immediate offsets)
   int shm_lit_smem = 0;      // JIT fp64: diagonal-run element factors read from a shared-memory table
+  int shm_autotune = 1;      // JIT fp64: time both tile pipelines per launch in the first runs, keep the faster
   int async = 0;             // run / set_state / get_state (contiguous layouts) return without a stream sync
   int zero_skip = 1;         // runs from |0...0>: tiles provably zero in and out are not visited
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter

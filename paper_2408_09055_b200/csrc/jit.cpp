@@ -271,6 +271,7 @@ static bool tma_dims(const ShmLaunch &sl, TmaDims &d) {
   return true;
 }
 thread_local bool g_no_tma = false;
+thread_local int g_force_pipe = -1;  // autotune: -1 = the option, 0/1 = forced
 struct TmaRetry {};
 
 // The straight-line source of one shared-memory launch (same skeleton as
@@ -720,7 +721,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // mirror, |a0 - 1| = 2e-6).
   // (two groups of 256: the fp64 2^12 tiles; fp32's 2 x 512 threads at 64
   // registers measured slower than two single-buffer CTAs)
-  bool pipe = nbuf == 1 && C->opt.shm_pipe && 2 * NT <= 512 &&
+  bool pipe = nbuf == 1 && (g_force_pipe >= 0 ? g_force_pipe != 0 : C->opt.shm_pipe != 0) && 2 * NT <= 512 &&
               layout(3, off_jtab, off_stab, off_btab, off_mbar) + 1024 <= 233472;
   if (tma && !pipe) throw TmaRetry();
   // the thread-factor table must not cost occupancy (or exceed the opt-in
@@ -1572,27 +1573,49 @@ static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &s
 
 // Generate and compile the specialised kernel of every L_SHM launch of the
 // plan (all simulated ranks); Launch::jit points at the cache entry.
+// Autotuning (option shm_autotune): a launch whose kernel can run either
+// tile pipeline (one CTA of two thread groups on a ring of three buffers,
+// or two single-buffer CTAs per SM) gets both compiled; runtime.cu times
+// each once in the first runs after the plan and keeps the faster per
+// launch (measured per-launch differences of up to 10% either way, not
+// predictable from the phase count).
 void shm_jit_prepare(atlas_ctx *C) {
   std::vector<std::string> srcs, names;
-  std::vector<Launch *> lns;
+  std::vector<std::pair<Launch *, int>> lns;  // (launch, 0 = primary / 1 = alternative)
+  auto add = [&](Launch *ln, int which, int force) {
+    g_force_pipe = force;
+    std::string body;
+    try {
+      body = shm_jit_source(C, ln->sl, "atlas_shm_jit");
+    } catch (...) {
+      g_force_pipe = -1;
+      throw;
+    }
+    g_force_pipe = -1;
+    // the name does not enter the cache key: it is derived from the body
+    const size_t h = std::hash<std::string>()(body);
+    char nm[64];
+    snprintf(nm, sizeof nm, "atlas_shm_%016zx", h);
+    std::string s = body;
+    const size_t at = s.find("atlas_shm_jit");
+    s.replace(at, strlen("atlas_shm_jit"), nm);
+    for (size_t i = 0; i < srcs.size(); i++)
+      if (lns[i].first == ln && srcs[i] == s) return;  // both variants are the same kernel
+    srcs.push_back(s);
+    names.push_back(nm);
+    lns.push_back({ln, which});
+  };
   for (auto &P : C->prog)
     for (auto &ln : P)
       if (ln.type == L_SHM) {
-        // the name does not enter the cache key: it is derived from the body
-        std::string body = shm_jit_source(C, ln.sl, "atlas_shm_jit");
-        const size_t h = std::hash<std::string>()(body);
-        char nm[64];
-        snprintf(nm, sizeof nm, "atlas_shm_%016zx", h);
-        std::string s = body;
-        const size_t at = s.find("atlas_shm_jit");
-        s.replace(at, strlen("atlas_shm_jit"), nm);
-        srcs.push_back(s);
-        names.push_back(nm);
-        lns.push_back(&ln);
+        ln.jit_alt = nullptr;
+        ln.tune_ms[0] = ln.tune_ms[1] = -1.f;
+        add(&ln, 0, -1);
+        if (C->opt.shm_autotune && C->dt == ATLAS_C128 && C->opt.shm_pipe) add(&ln, 1, 0);
       }
   if (srcs.empty()) return;
   auto ents = jit_compile_all(srcs, names);
-  for (size_t i = 0; i < lns.size(); i++) lns[i]->jit = ents[i];
+  for (size_t i = 0; i < lns.size(); i++) (lns[i].second ? lns[i].first->jit_alt : lns[i].first->jit) = ents[i];
 }
 
 static int g_nsms = 0;

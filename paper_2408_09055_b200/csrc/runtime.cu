@@ -678,6 +678,14 @@ void run(atlas_ctx *C) {
   const int S = C->sp.s;
   std::vector<size_t> pc(C->nslots, 0);
   std::vector<char> fused_x(S + 1, 0);  // remap k's exchange done by the launches (fused)
+  // autotuning (jit.cpp shm_jit_prepare): launches with two pipeline
+  // variants run the one not yet timed, between two events
+  struct Tune {
+    Launch *ln;
+    int which;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Tune> tunes;
   const double2 *mats = (const double2 *)C->d_mats;
   for (int k = 0; k < S; k++) {
     if (k > 0 && C->exch[k].gp > 0 && fused_x[k]) {
@@ -760,7 +768,15 @@ void run(atlas_ctx *C) {
             void *peers[8] = {nullptr};
             if (operm && sl.peer_gp > 0 && ln.jit) fill_peers(C, k + 1, s, peers, pex);
             if (pex) fused_x[k + 1] = 1;
-            if (ln.jit) {
+            if (ln.jit && ln.jit_alt) {
+              Tune t{const_cast<Launch *>(&ln), ln.tune_ms[0] < 0 ? 0 : 1, nullptr, nullptr};
+              CK(cudaEventCreate(&t.e0));
+              CK(cudaEventCreate(&t.e1));
+              CK(cudaEventRecord(t.e0, C->stream));
+              CK(launch_shm_jit(t.which ? ln.jit_alt : ln.jit, st, dst, sl, C->stream, zm, skip, peers));
+              CK(cudaEventRecord(t.e1, C->stream));
+              tunes.push_back(t);
+            } else if (ln.jit) {
               CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm, skip, peers));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
@@ -780,7 +796,19 @@ void run(atlas_ctx *C) {
       }
     }
   }
-  if (!C->opt.async || timing) CK(cudaStreamSynchronize(C->stream));  // async: the caller syncs its stream
+  if (!C->opt.async || timing || !tunes.empty())
+    CK(cudaStreamSynchronize(C->stream));  // async: the caller syncs its stream
+  for (Tune &t : tunes) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, t.e0, t.e1));
+    cudaEventDestroy(t.e0);
+    cudaEventDestroy(t.e1);
+    t.ln->tune_ms[t.which] = ms;
+    if (t.ln->tune_ms[0] >= 0 && t.ln->tune_ms[1] >= 0) {  // both timed: keep the faster
+      if (t.ln->tune_ms[1] < t.ln->tune_ms[0]) std::swap(t.ln->jit, t.ln->jit_alt);
+      t.ln->jit_alt = nullptr;
+    }
+  }
   if (timing) {
     for (size_t i = 0; i < rec.size(); i++) {
       float ms = 0;
