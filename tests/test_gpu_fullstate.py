@@ -248,3 +248,49 @@ def test_zero_skip_virtual_world_ranks(W):
     for zs in (1, 0):
         (psi,), _ = run(c, world=W, zero_skip=zs)
         check(psi, ref)
+
+
+def test_async_two_contexts_pipelined():
+    """Option async (bench.py's e2e pipeline): two contexts of one circuit on
+    two torch streams; each step uploads an input (atlas_set_state), runs
+    and reads the result back (atlas_get_state) without a host sync; the
+    caller synchronises the stream before reusing a context's buffers.
+    Every step's result element-wise vs O1 (alternating inputs: |0...0> and
+    an arbitrary state)."""
+    torch = pytest.importorskip("torch")
+    n = 18
+    c = C.make("su2random", n)
+    rng = np.random.default_rng(5)
+    psi1 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi1 /= np.linalg.norm(psi1)
+    psi0 = np.zeros(1 << n, dtype=np.complex128)
+    psi0[0] = 1
+    refs = [O.simulate(c), O.simulate(c, init=psi1)]
+    ins = [torch.from_numpy(p.view(np.float64).copy()).pin_memory() for p in (psi0, psi1)]
+    outs = [torch.empty(2 << n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    sims = [A.Simulator(n, 0, 1, 0) for _ in range(2)]
+    try:
+        for s, st in zip(sims, streams):
+            s.set_stream(st.cuda_stream)
+            s.load_circuit(c.gates)
+            s.plan()
+            s.set_option("init", 0)
+            s.set_option("async", 1)
+        pending = [None, None]
+        for step in range(6):
+            j = step % 2
+            streams[j].synchronize()
+            if pending[j] is not None:
+                check(outs[j].numpy().view(np.complex128), refs[pending[j]])
+            k = step % 2 if step < 2 else (step // 2) % 2
+            sims[j].set_state_from(ins[k].data_ptr(), 0, 1 << n)
+            sims[j].run()
+            sims[j].get_state_into(outs[j].data_ptr(), 0, 1 << n)
+            pending[j] = k
+        for j in range(2):
+            streams[j].synchronize()
+            check(outs[j].numpy().view(np.complex128), refs[pending[j]])
+    finally:
+        for s in sims:
+            s.close()
