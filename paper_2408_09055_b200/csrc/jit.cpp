@@ -779,6 +779,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
     << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl"
     << (tma ? ", const TMap *__restrict__ tmg" : "") << (pgp ? ", const PeerTab ptab" : "") << ") {\n";
+  if (pgp) o << "  __shared__ T *pts[8];\n";
   if (tma) {
     o << "  extern __shared__ __align__(1024) unsigned char smraw_[];\n";
     o << "  const unsigned smpad = (1024u - ((unsigned)__cvta_generic_to_shared(smraw_) & 1023u)) & 1023u;\n";
@@ -899,10 +900,14 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   o << "\n";
   o << "  const unsigned sm_base = (unsigned)__cvta_generic_to_shared(buf);\n";
   o << "//@LT_FILL@\n";
+  if (pgp) o << "  if (threadIdx.x < " << (1 << pgp) << ") pts[threadIdx.x] = ptab.p[threadIdx.x];\n";
   o << "  __syncthreads();\n";
-  if (pgp)
-    o << "  auto pst = [&](u64 y) -> T & { return ptab.p[y >> " << PSH << "][y & " << u64lit((1ull << PSH) - 1)
-      << "]; };\n";
+  // fused exchange: the destination blocks in shared memory (a run-time
+  // index into the parameter array would go through local memory); a
+  // store picks its block once per tile from the bits of its offset that
+  // are uniform over the tile and thread, XOR / OR the element's constant
+  // high bits
+  if (pgp) o << "  T *const *ptab_s = reinterpret_cast<T *const *>(pts);\n";
   o << "  auto tile_base = [&](u64 tile) { return btab[tile & 255]";
   for (int c = 1; c < nbt; c++) o << " | btab[" << 256 * c << " + ((tile >> " << 8 * c << ") & 255)]";
   o << "; };\n";
@@ -1038,7 +1043,19 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     z << "      T zz; zz.x = 0; zz.y = 0;\n";
     if (pgp) {
       z << "      const u64 gy = obase + ooff_t;\n";
-      for (int it = 0; it < NE; it++) z << "      pst(gy + " << u64lit(PB(itoff[it])) << ") = zz;\n";
+      std::map<uint64_t, int> blk;
+      for (int it = 0; it < NE; it++) {
+        const uint64_t c = PB(itoff[it]) >> PSH;
+        if (!blk.count(c)) {
+          const int k = (int)blk.size();
+          blk[c] = k;
+          z << "      T *zd" << k << " = ptab_s[(int)(gy >> " << PSH << ") | " << c << "] + (gy & "
+            << u64lit((1ull << PSH) - 1) << ");\n";
+        }
+      }
+      for (int it = 0; it < NE; it++)
+        z << "      zd" << blk[PB(itoff[it]) >> PSH] << "[" << u64lit(PB(itoff[it]) & ((1ull << PSH) - 1))
+          << "] = zz;\n";
     } else {
       z << (operm ? "      T *g = dst + obase + ooff_t;\n" : "      T *g = st + base + off_t;\n");
       for (int it = 0; it < NE; it++) z << "      g[" << u64lit(PB(itoff[it])) << "] = zz;\n";
@@ -1408,12 +1425,28 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
           o << "      if ((base & " << u64lit(terms[i].base_mask) << ") == " << u64lit(terms[i].base_val)
             << ") cg ^= " << u64lit(PB(terms[i].gvec)) << ";\n";
       }
+      std::map<uint64_t, int> blk;
+      if (pgp) {
+        o << "      const u64 yb = obase | cg; const int bt = (int)(yb >> " << PSH << ");\n";
+        for (int e = 0; e < NE; e++) {
+          uint64_t x = 0;
+          for (int i = 0; i < RB; i++)
+            if ((e >> i) & 1) x ^= limg[i];
+          const uint64_t c = PB(x) >> PSH;
+          if (!blk.count(c)) {
+            const int k = (int)blk.size();
+            blk[c] = k;
+            o << "      T *pd" << k << " = ptab_s[bt ^ " << c << "];\n";
+          }
+        }
+      }
       for (int e = 0; e < NE; e++) {
         uint64_t x = 0;
         for (int i = 0; i < RB; i++)
           if ((e >> i) & 1) x ^= limg[i];
         if (pgp)
-          o << "      pst(obase | (cg ^ " << u64lit(PB(x)) << ")) = v[" << e << "];\n";
+          o << "      pd" << blk[PB(x) >> PSH] << "[(yb ^ " << u64lit(PB(x)) << ") & " << u64lit((1ull << PSH) - 1)
+            << "] = v[" << e << "];\n";
         else
           o << "      " << (operm ? "dst[obase" : "st[base") << " | (cg ^ " << u64lit(PB(x)) << ")] = v[" << e << "];\n";
       }
@@ -1444,10 +1477,25 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
     o << "      " << GS << "\n    }\n";
   }
   if (!ld) {
-    if (pgp) o << "    { const u64 gy = obase + ooff_t;\n";
-    else o << (operm ? "    { T *g = dst + obase + ooff_t;\n" : "    { T *g = st + base + off_t;\n");
+    std::map<uint64_t, int> oblk;
+    if (pgp) {
+      o << "    { const u64 gy = obase + ooff_t;\n";
+      for (int it = 0; it < NE; it++) {
+        const uint64_t c = PB(itoff[it]) >> PSH;
+        if (!oblk.count(c)) {
+          const int k = (int)oblk.size();
+          oblk[c] = k;
+          o << "      T *od" << k << " = ptab_s[(int)(gy >> " << PSH << ") | " << c << "] + (gy & "
+            << u64lit((1ull << PSH) - 1) << ");\n";
+        }
+      }
+    } else {
+      o << (operm ? "    { T *g = dst + obase + ooff_t;\n" : "    { T *g = st + base + off_t;\n");
+    }
     auto gst = [&](int it) {
-      return pgp ? "pst(gy + " + u64lit(PB(itoff[it])) + ")" : "g[" + u64lit(PB(itoff[it])) + "]";
+      return pgp ? "od" + std::to_string(oblk[PB(itoff[it]) >> PSH]) + "[" +
+                       u64lit(PB(itoff[it]) & ((1ull << PSH) - 1)) + "]"
+                 : "g[" + u64lit(PB(itoff[it])) + "]";
     };
     if (early) {
       std::vector<int> as;
