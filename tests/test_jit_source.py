@@ -123,3 +123,22 @@ def test_fold_leading_permutation_phase():
     for i in folded:
         assert "#define ZERO_OK 0" in on[i]
         assert on[i].count("{ // phase ") == off[i].count("{ // phase ") - 1
+
+
+def test_fused_exchange_kernels_compile(tmp_path):
+    """The last shared-memory launch of each stage of a W = 8 plan carries
+    the exchange (ATLAS_PEER: stores into the destination ranks' blocks);
+    it compiles for sm_100a without spills and picks its destination block
+    from the shared-memory table once per tile (no per-store local-memory
+    pointer load)."""
+    c = C.su2random(20)
+    with A.Simulator(c.n, 0, 8, 0, virtual_world=1) as s:
+        s.load_circuit(c.gates)
+        s.plan()
+        srcs = [s.jit_source(i, 3) for i in range(s.plan_stats()["shm_kernels"])]
+    peer = [src for src in srcs if "#define ATLAS_PEER" in src]
+    assert peer
+    for i, src in enumerate(peer):
+        assert "ptab_s[" in src and "ptab.p[threadIdx.x]" in src
+        regs, spill = ptxas(src, tmp_path, f"x{i}")
+        assert spill == 0
