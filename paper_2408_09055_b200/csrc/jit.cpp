@@ -1050,7 +1050,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
           const int k = (int)blk.size();
           blk[c] = k;
           z << "      T *zd" << k << " = ptab_s[(int)(gy >> " << PSH << ") | " << c << "] + (gy & "
-            << u64lit((1ull << PSH) - 1) << ");\n";
+            << u64lit((1ull << PSH) - 1) << "); __builtin_assume(__isGlobal(zd" << k << "));\n";
         }
       }
       for (int it = 0; it < NE; it++)
@@ -1436,7 +1436,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
           if (!blk.count(c)) {
             const int k = (int)blk.size();
             blk[c] = k;
-            o << "      T *pd" << k << " = ptab_s[bt ^ " << c << "];\n";
+            o << "      T *pd" << k << " = ptab_s[bt ^ " << c << "]; __builtin_assume(__isGlobal(pd" << k << "));\n";
           }
         }
       }
@@ -1486,7 +1486,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
           const int k = (int)oblk.size();
           oblk[c] = k;
           o << "      T *od" << k << " = ptab_s[(int)(gy >> " << PSH << ") | " << c << "] + (gy & "
-            << u64lit((1ull << PSH) - 1) << ");\n";
+            << u64lit((1ull << PSH) - 1) << "); __builtin_assume(__isGlobal(od" << k << "));\n";
         }
       }
     } else {
