@@ -47,7 +47,7 @@ def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=5)  # >= 4: the autotuning runs
     p.add_argument("--workload", default="su2random_n28")
     p.add_argument("--impl", default="atlas", choices=["atlas", "reference"])
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])

@@ -217,11 +217,12 @@ const char *atlas_last_error(void);
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
  *   "shm_autotune"   plan-specialised fp64 kernels: every shared-memory launch
- *                    that can run either tile pipeline (two thread groups on
- *                    a ring of three buffers, or two single-buffer CTAs per
- *                    SM) has both compiled; the first two atlas_run calls
- *                    after a plan time one each (CUDA events) and the faster
- *                    is kept for that launch [1]
+ *                    gets up to four variants compiled (tile pipeline: two
+ *                    thread groups on a ring of three buffers or two
+ *                    single-buffer CTAs per SM; last phase stored straight
+ *                    to HBM or through shared memory); the first atlas_run
+ *                    calls after a plan time one variant each (CUDA events)
+ *                    and the fastest is kept for that launch [1]
  *   "async"          1 = atlas_run, and atlas_set_state / atlas_get_state
  *                    when the layout is the identity (contiguous copies),
  *                    return once the work is enqueued on the context's

@@ -22,10 +22,12 @@ struct Launch {
   double sre = 1, sim = 0;   // L_SCALE
   int64_t bytes = 0;         // algorithmic HBM bytes
   void *jit = nullptr;       // L_SHM: plan-specialised kernel (jit.cpp), or null
-  // autotuning (option shm_autotune): the other pipeline variant of the same
-  // launch and the device time each variant took in the tuning runs
-  void *jit_alt = nullptr;
-  float tune_ms[2] = {-1.f, -1.f};
+  // autotuning (option shm_autotune): the variants of the same launch (tile
+  // pipeline x direct last-phase store; variant 0 = the defaults) and the
+  // device time each took in the tuning runs; nvar = 0 once tuned
+  void *jit_var[4] = {nullptr, nullptr, nullptr, nullptr};
+  float tune_ms[4] = {-1.f, -1.f, -1.f, -1.f};
+  int nvar = 0;
 };
 
 // Exchange of one remap (stage boundary k-1 -> k): swap the g' top local

@@ -272,6 +272,7 @@ static bool tma_dims(const ShmLaunch &sl, TmaDims &d) {
 }
 thread_local bool g_no_tma = false;
 thread_local int g_force_pipe = -1;  // autotune: -1 = the option, 0/1 = forced
+thread_local int g_force_ld = -1;    // autotune: 0 = no direct last-phase store
 struct TmaRetry {};
 
 // The straight-line source of one shared-memory launch (same skeleton as
@@ -462,7 +463,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       Ac0[p] = Sx(GL, ph[p].c0_swz);
     }
   const int lastp = sl.nphase - 1;
-  const bool ld_ = sl.last_direct != 0;
+  const bool ld_ = sl.last_direct != 0 && g_force_ld != 0;
   // fold0: a leading phase with no op but its folded permutation (a CX
   // block whose dense gates come later) only moves the tile through shared
   // memory once more; its permuted store is folded into the tile load
@@ -1005,7 +1006,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   };
 
   const int last = sl.nphase - 1;
-  const bool ld = sl.last_direct != 0;
+  const bool ld = ld_;
   if (ld) {
     o << "  u64 gthr = 0;\n  { const int jtl = (int)(jtab[" << jslot[last] * NT << " + tid] & 0xffffu);";
     for (int b = 0; b < K; b++)
@@ -1629,17 +1630,20 @@ static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &s
 // predictable from the phase count).
 void shm_jit_prepare(atlas_ctx *C) {
   std::vector<std::string> srcs, names;
-  std::vector<std::pair<Launch *, int>> lns;  // (launch, 0 = primary / 1 = alternative)
-  auto add = [&](Launch *ln, int which, int force) {
-    g_force_pipe = force;
+  std::vector<std::pair<Launch *, int>> lns;  // (launch, variant index)
+  auto add = [&](Launch *ln, int force_pipe, int force_ld) {
+    g_force_pipe = force_pipe;
+    g_force_ld = force_ld;
     std::string body;
     try {
       body = shm_jit_source(C, ln->sl, "atlas_shm_jit");
     } catch (...) {
       g_force_pipe = -1;
+      g_force_ld = -1;
       throw;
     }
     g_force_pipe = -1;
+    g_force_ld = -1;
     // the name does not enter the cache key: it is derived from the body
     const size_t h = std::hash<std::string>()(body);
     char nm[64];
@@ -1648,22 +1652,37 @@ void shm_jit_prepare(atlas_ctx *C) {
     const size_t at = s.find("atlas_shm_jit");
     s.replace(at, strlen("atlas_shm_jit"), nm);
     for (size_t i = 0; i < srcs.size(); i++)
-      if (lns[i].first == ln && srcs[i] == s) return;  // both variants are the same kernel
+      if (lns[i].first == ln && srcs[i] == s) return;  // the same kernel as a variant already listed
     srcs.push_back(s);
     names.push_back(nm);
-    lns.push_back({ln, which});
+    lns.push_back({ln, ln->nvar++});
   };
   for (auto &P : C->prog)
     for (auto &ln : P)
       if (ln.type == L_SHM) {
-        ln.jit_alt = nullptr;
-        ln.tune_ms[0] = ln.tune_ms[1] = -1.f;
-        add(&ln, 0, -1);
-        if (C->opt.shm_autotune && C->dt == ATLAS_C128 && C->opt.shm_pipe) add(&ln, 1, 0);
+        ln.nvar = 0;
+        for (int v = 0; v < 4; v++) {
+          ln.jit_var[v] = nullptr;
+          ln.tune_ms[v] = -1.f;
+        }
+        add(&ln, -1, -1);
+        if (C->opt.shm_autotune && C->dt == ATLAS_C128) {
+          if (C->opt.shm_pipe) add(&ln, 0, -1);
+          if (ln.sl.last_direct) {
+            add(&ln, -1, 0);
+            if (C->opt.shm_pipe) add(&ln, 0, 0);
+          }
+        }
       }
   if (srcs.empty()) return;
   auto ents = jit_compile_all(srcs, names);
-  for (size_t i = 0; i < lns.size(); i++) (lns[i].second ? lns[i].first->jit_alt : lns[i].first->jit) = ents[i];
+  for (size_t i = 0; i < lns.size(); i++) lns[i].first->jit_var[lns[i].second] = ents[i];
+  for (auto &P : C->prog)
+    for (auto &ln : P)
+      if (ln.type == L_SHM) {
+        ln.jit = ln.jit_var[0];
+        if (ln.nvar < 2) ln.nvar = 0;  // nothing to tune
+      }
 }
 
 static int g_nsms = 0;

@@ -768,12 +768,14 @@ void run(atlas_ctx *C) {
             void *peers[8] = {nullptr};
             if (operm && sl.peer_gp > 0 && ln.jit) fill_peers(C, k + 1, s, peers, pex);
             if (pex) fused_x[k + 1] = 1;
-            if (ln.jit && ln.jit_alt) {
-              Tune t{const_cast<Launch *>(&ln), ln.tune_ms[0] < 0 ? 0 : 1, nullptr, nullptr};
+            if (ln.jit && ln.nvar > 1) {
+              int w = 0;
+              while (w < ln.nvar - 1 && ln.tune_ms[w] >= 0) w++;
+              Tune t{const_cast<Launch *>(&ln), w, nullptr, nullptr};
               CK(cudaEventCreate(&t.e0));
               CK(cudaEventCreate(&t.e1));
               CK(cudaEventRecord(t.e0, C->stream));
-              CK(launch_shm_jit(t.which ? ln.jit_alt : ln.jit, st, dst, sl, C->stream, zm, skip, peers));
+              CK(launch_shm_jit(ln.jit_var[w], st, dst, sl, C->stream, zm, skip, peers));
               CK(cudaEventRecord(t.e1, C->stream));
               tunes.push_back(t);
             } else if (ln.jit) {
@@ -803,10 +805,14 @@ void run(atlas_ctx *C) {
     CK(cudaEventElapsedTime(&ms, t.e0, t.e1));
     cudaEventDestroy(t.e0);
     cudaEventDestroy(t.e1);
-    t.ln->tune_ms[t.which] = ms;
-    if (t.ln->tune_ms[0] >= 0 && t.ln->tune_ms[1] >= 0) {  // both timed: keep the faster
-      if (t.ln->tune_ms[1] < t.ln->tune_ms[0]) std::swap(t.ln->jit, t.ln->jit_alt);
-      t.ln->jit_alt = nullptr;
+    Launch *L = t.ln;
+    L->tune_ms[t.which] = ms;
+    if (t.which == L->nvar - 1) {  // every variant timed: keep the fastest
+      int best = 0;
+      for (int v = 1; v < L->nvar; v++)
+        if (L->tune_ms[v] < L->tune_ms[best]) best = v;
+      L->jit = L->jit_var[best];
+      L->nvar = 0;
     }
   }
   if (timing) {
