@@ -10,7 +10,7 @@ fi
 for w in ${WORKLOADS:-su2random_n28}; do
 for opt in ${OPTS:--}; do
   a=""; [ "$opt" != "-" ] && a=$(for x in ${opt//,/ }; do echo --opt $x; done)
-  timeout 300 python bench.py --steps ${STEPS:-20} --warmup 3 --no-e2e --no-cpu --workload $w $a > $O/${T}_q.json 2> $O/${T}_q.err
+  timeout 300 python bench.py --steps ${STEPS:-20} --warmup 5 --no-e2e --no-cpu --workload $w $a > $O/${T}_q.json 2> $O/${T}_q.err
   python -c "
 import json
 d=json.loads(open('$O/${T}_q.json').read().strip().splitlines()[-1])
