@@ -216,8 +216,8 @@ const char *atlas_last_error(void);
  *                    literals materialised by UMOV pairs; ptxas hoists the
  *                    loads out of the tile loop and spills at the
  *                    128-register cap, so it is off by default [0]
- *   "shm_autotune"   plan-specialised fp64 kernels: every shared-memory launch
- *                    gets up to four variants compiled (tile pipeline: two
+ *   "shm_autotune"   plan-specialised kernels: every shared-memory launch
+ *                    gets up to four variants compiled (fp64 tile pipeline: two
  *                    thread groups on a ring of three buffers or two
  *                    single-buffer CTAs per SM; last phase stored straight
  *                    to HBM or through shared memory); the first atlas_run

@@ -1666,7 +1666,9 @@ void shm_jit_prepare(atlas_ctx *C) {
           ln.tune_ms[v] = -1.f;
         }
         add(&ln, -1, -1);
-        if (C->opt.shm_autotune && C->dt == ATLAS_C128) {
+        if (C->opt.shm_autotune) {
+          // (fp32 tiles never use the two-group pipeline: the pipeline
+          // variants then generate the same source and are dropped)
           if (C->opt.shm_pipe) add(&ln, 0, -1);
           if (ln.sl.last_direct) {
             add(&ln, -1, 0);
