@@ -230,6 +230,12 @@ const char *atlas_last_error(void);
  *                    caller synchronises that stream before it touches the
  *                    host buffers or the result (lets two contexts overlap
  *                    host<->device copies with compute) [0]
+ *   "zero_lazy"      with zero_skip: when every stage-0 launch until each
+ *                    local slot has been active is modelled by the tracking,
+ *                    the first launch stores only tile 0 (not the zeros) and
+ *                    later launches take the elements of the still-zero
+ *                    region as zero in their first gather; the launch that
+ *                    covers the last such slot rewrites the whole shard [1]
  *   "zero_skip"      1 = a run that starts from |0...0> tracks the local
  *                    slots no launch has made active yet (they are still 0):
  *                    an in-place plan-specialised shared-memory launch does

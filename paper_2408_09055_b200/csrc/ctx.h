@@ -98,6 +98,7 @@ struct Options {
   int shm_lit_smem = 0;      // JIT fp64: diagonal-run element factors read from a shared-memory table
   int shm_autotune = 1;      // JIT fp64: time both tile pipelines per launch in the first runs, keep the faster
   int async = 0;             // run / set_state / get_state (contiguous layouts) return without a stream sync
+  int zero_lazy = 1;         // with zero_skip: zeros of the |0...0> launch not stored, zero-filled on load
   int zero_skip = 1;         // runs from |0...0>: tiles provably zero in and out are not visited
   int shm_jit = 1;           // 1: plan-specialised SHM kernels (NVRTC); 0: interpreter
   long long dp_budget = 250000;

@@ -133,6 +133,10 @@ struct ShmLaunch {
   // destination blocks (the peers' other buffers, or this slot's own) passed
   // as a launch argument
   int32_t peer_gp;
+  // 1: the launch may run with lazy zeros (zfill != 0: it lies in stage 0
+  // between the |0...0> launch and the launch that makes every local slot
+  // active); only such kernels carry the zero-fill load code
+  int32_t zfill_cap;
 };
 
 // Fused dense kernel ("Fusion"): one 2^k x 2^k matrix on k slots.

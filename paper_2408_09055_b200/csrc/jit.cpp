@@ -471,7 +471,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   // (and re-swizzled) position -- and the phase is not emitted (option
   // shm_fold_perm; cp.async loads only, not when the phase's gather feeds a
   // direct HBM store)
-  const bool fold0 = C->opt.shm_fold_perm && nbuf == 1 && !tma && sl.nphase >= 1 && ph[0].permuted &&
+  const bool fold0 = C->opt.shm_fold_perm && nbuf == 1 && !tma && !sl.zfill_cap && sl.nphase >= 1 && ph[0].permuted &&
                      ph[0].op_begin == ph[0].op_end && !(ld_ && lastp == 0);
   std::vector<int> rmask(sl.nphase), gsw(sl.nphase, 0), ssw(sl.nphase, 0);
   std::vector<unsigned> qln(sl.nphase, 0xffff);
@@ -778,7 +778,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
          "if (!ok && clock64() - t0 > 20000000000ll) __trap(); } while (!ok); }\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << BT << ", " << minb << ") " << name
-    << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl"
+    << "(T *__restrict__ st, T *dst, int zmode, u64 nact, u32 ntl, u32 zfill"
     << (tma ? ", const TMap *__restrict__ tmg" : "") << (pgp ? ", const PeerTab ptab" : "") << ") {\n";
   if (pgp) o << "  __shared__ T *pts[8];\n";
   if (tma) {
@@ -938,7 +938,8 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   }
   for (int it = 0; it < NE; it++) {
     o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (swl ^ "
-      << ldimg((unsigned)(it * NT)) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it]) << "; ";
+      << ldimg((unsigned)(it * NT)) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it])
+      << "; ";
     if (!f32) o << "asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
     else o << "asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\\n\" ::\"r\"(sa), \"l\"(ga)); }\n";
   }
@@ -1040,7 +1041,11 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   std::string zero_tile;
   {
     std::ostringstream z;
-    z << "    if (zmode && (zmode == 1 || tile != 0)) {\n";
+    // zmode bit 2 (lazy zeros, runtime.cu): the zero tiles are not even
+    // stored -- every later launch that reads them zero-fills them (zfill)
+    // until a launch has rewritten the whole shard
+    z << "    if (zmode && ((zmode & 3) == 1 || tile != 0)) {\n";
+    z << "      if (!(zmode & 4)) {\n";
     z << "      T zz; zz.x = 0; zz.y = 0;\n";
     if (pgp) {
       z << "      const u64 gy = obase + ooff_t;\n";
@@ -1061,6 +1066,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       z << (operm ? "      T *g = dst + obase + ooff_t;\n" : "      T *g = st + base + off_t;\n");
       for (int it = 0; it < NE; it++) z << "      g[" << u64lit(PB(itoff[it])) << "] = zz;\n";
     }
+    z << "      }\n";
     if (pipe) z << "      " << next_issue << "\n";
     if (NB) z << "      itp ^= 1;\n";
     z << "      continue;\n    }\n";
@@ -1160,10 +1166,24 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       if (early && p == 0) {
         o << "      if (zmode) {\n";
         for (int e2 = 0; e2 < NE; e2++) o << "        v[" << e2 << "].x = 0; v[" << e2 << "].y = 0;\n";
-        o << "        if (zmode == 2 && tile == 0 && jt == 0) v[0].x = 1;\n      } else {\n";
+        o << "        if ((zmode & 3) == 2 && tile == 0 && jt == 0) v[0].x = 1;\n      } else {\n";
       }
       const auto ax = addr_group("sj", as, "      ");
-      for (int e = 0; e < NE; e++) o << "      v[" << e << "] = " << ax[e] << ";\n";
+      if (sl.zfill_cap && p == 0) {
+        // lazy zeros (zfill, launch argument: tile bits of active qubits
+        // still |0>): an element with such a bit set is taken as zero --
+        // the shard holds no zeros there, only what earlier runs left
+        o << "      const unsigned zt = (unsigned)jt & zfill;\n";
+        for (int e = 0; e < NE; e++) {
+          unsigned eb = 0;
+          for (int i = 0; i < RB; i++)
+            if ((e >> i) & 1) eb |= 1u << P.rbit[i];
+          o << "      if (zt | (" << eb << "u & zfill)) { v[" << e << "].x = 0; v[" << e << "].y = 0; } else v[" << e
+            << "] = " << ax[e] << ";\n";
+        }
+      } else {
+        for (int e = 0; e < NE; e++) o << "      v[" << e << "] = " << ax[e] << ";\n";
+      }
       if (early && p == 0) o << "      }\n";
     }
     if (early && ld && p == last) o << "      " << GS << "\n      " << next_issue << "\n";
@@ -1622,11 +1642,36 @@ static std::vector<JitEntry *> jit_compile_all(const std::vector<std::string> &s
 
 // Generate and compile the specialised kernel of every L_SHM launch of the
 // plan (all simulated ranks); Launch::jit points at the cache entry.
-// Autotuning (option shm_autotune): a launch whose kernel can run either
-// tile pipeline (one CTA of two thread groups on a ring of three buffers,
-// or two single-buffer CTAs per SM) gets both compiled; runtime.cu times
-// each once in the first runs after the plan and keeps the faster per
-// launch (measured per-launch differences of up to 10% either way, not
+// Lazy-zero chains (runtime.cu): the stage-0 launches after the first, up to
+// the one that makes every local slot active, carry the zero-fill load; the
+// chain holds only if every launch in it is an in-place shared-memory launch.
+void shm_mark_zfill(atlas_ctx *C) {
+  const uint64_t lmask = C->L >= 64 ? ~0ull : (1ull << C->L) - 1;
+  for (auto &P : C->prog) {
+    for (auto &ln : P) ln.sl.zfill_cap = 0;
+    if (!C->opt.zero_skip || !C->opt.zero_lazy || C->opt.shm_tma || !C->opt.shm_jit) continue;
+    uint64_t z = lmask;
+    bool ok = false;
+    size_t i = 0;
+    for (; i < P.size() && P[i].stage == 0; i++) {
+      if (P[i].type != L_SHM || P[i].sl.out_perm_off >= 0) break;
+      z &= P[i].sl.nonactive;
+      if (!z) {
+        ok = true;
+        break;
+      }
+    }
+    if (ok)
+      for (size_t j = 1; j <= i; j++) P[j].sl.zfill_cap = 1;
+  }
+}
+
+// Autotuning (option shm_autotune): every shared-memory launch gets up to
+// four variants compiled -- tile pipeline (one CTA of two thread groups on a
+// ring of three buffers, or two single-buffer CTAs per SM) x last phase
+// stored straight to HBM or copied out through shared memory; runtime.cu
+// times each once in the first runs after the plan and keeps the fastest per
+// launch (measured per-launch differences of up to 13% either way, not
 // predictable from the phase count).
 void shm_jit_prepare(atlas_ctx *C) {
   std::vector<std::string> srcs, names;
@@ -1657,6 +1702,7 @@ void shm_jit_prepare(atlas_ctx *C) {
     names.push_back(nm);
     lns.push_back({ln, ln->nvar++});
   };
+  shm_mark_zfill(C);
   for (auto &P : C->prog)
     for (auto &ln : P)
       if (ln.type == L_SHM) {
@@ -1695,7 +1741,7 @@ bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->z
 // skip: non-active slots whose tiles with a 1 there are zero in and out (the
 // launch runs in place); those tiles are not visited at all
 cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
-                           uint64_t skip, void *const *peers) {
+                           uint64_t skip, void *const *peers, uint64_t zq) {
   JitEntry *E = (JitEntry *)jit;
   const int NT = E->threads > 0 ? E->threads : 1 << (sl.K - sl.RB);
   if (E->attr_set < E->smem) {
@@ -1768,8 +1814,12 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
     if (!peers) return cudaErrorInvalidValue;
     for (int b = 0; b < (1 << sl.peer_gp); b++) ptab.p[b] = peers[b];
   }
-  void *args[8] = {&st, &dst, &zmode, &nact, &ntl};
-  int na = 5;
+  // zq: local slots still |0> with lazy zeros -> the active ones as tile bits
+  uint32_t zfill = 0;
+  for (int b = 0; b < sl.K; b++)
+    if ((zq >> sl.act[b]) & 1) zfill |= 1u << b;
+  void *args[8] = {&st, &dst, &zmode, &nact, &ntl, &zfill};
+  int na = 6;
   if (E->tma_rank) args[na++] = &tmg;
   if (sl.peer_gp > 0) args[na++] = &ptab;
   return cudaLaunchKernel((const void *)E->kern, dim3((unsigned)grid), dim3(NT), args,
@@ -1779,6 +1829,7 @@ cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, 
 // source of launch i of slot s (tests / inspection: atlas_get_jit_source)
 std::string shm_jit_source_of(const atlas_ctx *C, int slot, int i) {
   if (slot < 0 || slot >= (int)C->prog.size()) fail(ATLAS_E_INVALID, "slot out of range");
+  shm_mark_zfill(const_cast<atlas_ctx *>(C));  // the same flags the run compiles with
   int j = 0;
   for (auto &ln : C->prog[slot])
     if (ln.type == L_SHM && j++ == i) return shm_jit_source(C, ln.sl, "atlas_shm_jit");

@@ -35,7 +35,7 @@ cudaError_t launch_swap_regions(int dtype, void *a, void *b, uint64_t n, cudaStr
 cudaError_t launch_init(int dtype, void *st, int L, bool one, cudaStream_t s);
 void shm_jit_prepare(atlas_ctx *C);
 cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
-                           uint64_t skip, void *const *peers);
+                           uint64_t skip, void *const *peers, uint64_t zq);
 bool shm_jit_zero_ok(const void *jit);
 
 #define CK(x)                                                                              \
@@ -539,7 +539,7 @@ static void run_offload(atlas_ctx *C) {
             const bool operm = sl.out_perm_off >= 0;
             void *dst = operm ? C->d_work[w ^ 1] : st;
             if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z, 0, nullptr));
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, z, 0, nullptr, 0));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                             (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,
@@ -675,6 +675,32 @@ void run(atlas_ctx *C) {
         zq[s] = lmask;
         zall[s] = slot_rank(C, s) != 0;
       }
+  // lazy zeros (option zero_lazy): on a slot whose first launch synthesises
+  // |0...0> and whose following stage-0 launches are all modelled by the
+  // tracking until every local slot has been active, the zeros are never
+  // stored: the first launch writes only tile 0, and every later launch
+  // takes the elements of the still-zero region (an active slot in zq) as
+  // zero in its first gather instead of using what the shard holds there.  The launch that makes zq
+  // empty visits every tile and rewrites the whole shard, so the state is
+  // complete from there on.  Otherwise the zeros are stored (as above).
+  std::vector<char> lazy(C->nslots, 0);
+  if (C->opt.zero_skip && C->opt.zero_lazy && !C->opt.shm_tma)
+    for (int s = 0; s < C->nslots; s++) {
+      if (zmode[s] != 2) continue;
+      const auto &P = C->prog[s];
+      uint64_t z = lmask;
+      for (size_t i = 0; i < P.size() && P[i].stage == 0; i++) {
+        const Launch &ln = P[i];
+        if (ln.type != L_SHM || !ln.jit || ln.sl.out_perm_off >= 0) break;
+        if (i > 0 && !ln.sl.zfill_cap) break;  // compiled without the zero-fill load
+        z &= ln.sl.nonactive;
+        if (!z) {
+          lazy[s] = 1;
+          zmode[s] |= 4;
+          break;
+        }
+      }
+    }
   const int S = C->sp.s;
   std::vector<size_t> pc(C->nslots, 0);
   std::vector<char> fused_x(S + 1, 0);  // remap k's exchange done by the launches (fused)
@@ -735,8 +761,10 @@ void run(atlas_ctx *C) {
         void *st = cur_buf(C, s);
         // a launch that synthesises |0...0> only writes the shard
         const int zm = (k == 0 && pc[s] == 1 && ln.type == L_SHM && ln.jit) ? zmode[s] : 0;
-        // zero tiles of this launch (see zq above)
+        // zero tiles of this launch (see zq above); lazy zeros: the elements
+        // to zero-fill (active slots still in zq)
         uint64_t skip = 0;
+        const uint64_t zfill = (lazy[s] && !zm) ? zq[s] : 0;
         if (!zm && zq[s]) {
           if (ln.type == L_SHM && ln.jit && ln.sl.out_perm_off < 0) {
             if (zall[s]) continue;  // the whole shard is zero: nothing to do
@@ -747,11 +775,14 @@ void run(atlas_ctx *C) {
           }
         }
         if (ln.type == L_SHM && zq[s]) zq[s] &= ln.sl.nonactive;  // active slots may turn nonzero
-        if (zm || skip) {
-          // algorithmic bytes of the tiles visited (write-only from |0...0>)
-          const int64_t vis = (int64_t)(ln.sl.ntiles >> __builtin_popcountll(skip));
-          const int64_t b = (int64_t)((double)ln.bytes * (double)vis / (double)ln.sl.ntiles);
-          mark(ln.type, zm ? ln.bytes / 2 : b);
+        if (zm || skip || zfill) {
+          // algorithmic bytes of the tiles visited (write-only from |0...0>;
+          // lazy zeros: tile 0 only; zero-filled elements are still read
+          // with their tile and discarded)
+          const double vf = std::ldexp(1.0, -__builtin_popcountll(skip));
+          int64_t b = (int64_t)((double)ln.bytes * vf);
+          if (zm) b = (zm & 4) ? (int64_t)((double)ln.bytes / 2.0 / (double)ln.sl.ntiles) : ln.bytes / 2;
+          mark(ln.type, b);
         } else {
           mark(ln.type, ln.bytes);
         }
@@ -775,11 +806,11 @@ void run(atlas_ctx *C) {
               CK(cudaEventCreate(&t.e0));
               CK(cudaEventCreate(&t.e1));
               CK(cudaEventRecord(t.e0, C->stream));
-              CK(launch_shm_jit(ln.jit_var[w], st, dst, sl, C->stream, zm, skip, peers));
+              CK(launch_shm_jit(ln.jit_var[w], st, dst, sl, C->stream, zm, skip, peers, zfill));
               CK(cudaEventRecord(t.e1, C->stream));
               tunes.push_back(t);
             } else if (ln.jit) {
-              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm, skip, peers));
+              CK(launch_shm_jit(ln.jit, st, dst, sl, C->stream, zm, skip, peers, zfill));
             } else {
               CK(launch_shm(dt, st, sl, (const ShmOp *)C->d_ops, (const double *)C->d_coef,
                             (const ShmPhase *)C->d_phases, (const DiagEnt *)C->d_ents,

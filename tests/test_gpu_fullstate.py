@@ -294,3 +294,30 @@ def test_async_two_contexts_pipelined():
     finally:
         for s in sims:
             s.close()
+
+
+@pytest.mark.parametrize("lazy", [1, 0])
+def test_zero_lazy_partial_support(lazy):
+    """Lazy zeros need every local qubit to become active during stage 0;
+    a circuit that never touches the high qubits keeps the stored zeros
+    (the run falls back), one that does is exact with zero-filled loads.
+    Both element-wise vs O1, and followed by a run from an arbitrary input
+    on the same context."""
+    n = 20
+    low = C.random_circuit(14, 120, 9)                       # qubits 0..13 only
+    part = C.Circuit(n, list(low.gates), "low14_in_20", 9)
+    full = C.make("su2random", n)
+    rng = np.random.default_rng(2)
+    psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi /= np.linalg.norm(psi)
+    for c in (part, full):
+        with A.Simulator(n, 0, 1, 0, zero_lazy=lazy, shm_grid=5) as s:
+            s.load_circuit(c.gates)
+            s.plan()
+            for _ in range(2):
+                s.run()
+                check(s.get_state(), O.simulate(c))
+            s.set_state(psi)
+            s.set_option("init", 0)
+            s.run()
+            check(s.get_state(), O.simulate(c, init=psi))

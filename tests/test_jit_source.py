@@ -83,10 +83,10 @@ def test_jit_source_reflects_program():
             assert "#define ZERO_OK 0" in src
             continue
         assert "#define ZERO_OK 1" in src
-        assert "zmode == 2 && tile == 0 && jt == 0" in src
+        assert "(zmode & 3) == 2 && tile == 0 && jt == 0" in src
         # zero tiles of a zmode launch: stored as zeros, no phases (linearity;
         # a shared-memory kernel keeps every tile inside itself)
-        assert "if (zmode && (zmode == 1 || tile != 0)) {" in src
+        assert "if (zmode && ((zmode & 3) == 1 || tile != 0)) {" in src
         # shared-memory addresses: one pointer per distinct low (bank) part
         assert re.search(r"T \*q\d+ = tb \+ \(sj \^ \d+\);", src)
     # plan-specialised: no op-program interpretation in the generated code
