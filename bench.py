@@ -554,6 +554,10 @@ def run_atlas(args):
                    "remap_ms_per_step": round(remap_ms, 4),
                    "kernels_ms_per_step_total": round(step_kernel_ms, 4),
                    "zero_skip": bool(extra.get("zero_skip", 1)),
+                   "zero_skip_note": ("exact, not an approximation: a run from |0...0> does not visit "
+                                      "tiles (or store zeros) it proves zero from the qubits no launch "
+                                      "has touched yet; without_zero_skip re-times the same steps with "
+                                      "zero_skip (and lazy zeros) off"),
                    "without_zero_skip": no_skip},
         "roofline": roof,
         "nvlink": nvlink,
