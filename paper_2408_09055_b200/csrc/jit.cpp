@@ -936,7 +936,15 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   } else {
     o << "    const int swl = sw_tid;\n";
   }
+  // lazy zeros: elements the first gather takes as zero need no load; the
+  // warp-uniform and element parts of that test skip whole cp.async
+  // instructions without per-thread state (the gather's per-element test
+  // covers the rest)
+  // (fp64 only: fp32 kernels have no register to spare at the 64 cap)
+  const bool zskip_ld = sl.zfill_cap && !f32;
+  if (zskip_ld) o << "    const bool zw = ((unsigned)tid & ~31u & zfill) != 0u;\n";
   for (int it = 0; it < NE; it++) {
+    if (zskip_ld) o << "    if (!zw && !(" << (it << (K - RB)) << "u & zfill))";
     o << "    { const unsigned sa = sm_base + (unsigned)((bsel * " << TILE << " + (swl ^ "
       << ldimg((unsigned)(it * NT)) << ")) * " << esz << "); const T *ga = g + " << u64lit(itoff[it])
       << "; ";
