@@ -777,10 +777,15 @@ void run(atlas_ctx *C) {
         if (ln.type == L_SHM && zq[s]) zq[s] &= ln.sl.nonactive;  // active slots may turn nonzero
         if (zm || skip || zfill) {
           // algorithmic bytes of the tiles visited (write-only from |0...0>;
-          // lazy zeros: tile 0 only; zero-filled elements are still read
-          // with their tile and discarded)
+          // lazy zeros: tile 0 only; an fp64 chain launch does not load the
+          // elements whose warp (tile bits >= 5) or register part has a
+          // still-zero qubit -- jit.cpp issue_load)
           const double vf = std::ldexp(1.0, -__builtin_popcountll(skip));
-          int64_t b = (int64_t)((double)ln.bytes * vf);
+          int zb = 0;
+          if (zfill && C->dt == ATLAS_C128 && ln.sl.zfill_cap)
+            for (int t = 5; t < ln.sl.K; t++) zb += (int)((zfill >> ln.sl.act[t]) & 1);
+          const double rf = std::ldexp(1.0, -zb);
+          int64_t b = (int64_t)((double)ln.bytes * vf * (1.0 + rf) / 2.0);
           if (zm) b = (zm & 4) ? (int64_t)((double)ln.bytes / 2.0 / (double)ln.sl.ntiles) : ln.bytes / 2;
           mark(ln.type, b);
         } else {
