@@ -413,6 +413,17 @@ def run_atlas(args):
                 "launches_per_step": cnt / args.steps, "avg_launch_ms": round(avg_ms, 4),
                 "share_of_step": round(tot_ms / args.steps / ms_step, 4),
                 "bytes_per_launch": int(bytes_per)}
+        # the launches that move the full shard (read + write every
+        # amplitude): the zero-skip / lazy-zero launches move far fewer bytes
+        # while still computing, which lowers the aggregate above
+        full_b = 2 * (16 if dtype == A.C128 else 8) * 2 ** (n - int(math.log2(world)))
+        dense = [(t, b) for k, t, b in launches if k == dom and b == full_b]
+        if dense:
+            dt_ = sum(t for t, _ in dense) / len(dense)
+            roof["full_pass_launches"] = {
+                "per_step": len(dense) / args.steps, "avg_launch_ms": round(dt_, 4),
+                "achieved": round(full_b / (dt_ / 1e3) / 1e9, 1),
+                "frac": round(full_b / (dt_ / 1e3) / 1e9 / peak, 4)}
     kinds_ms = {k: round(v[0] / args.steps, 4) for k, v in by.items()}
     remap_ms = sum(t for k, t, b in launches if k == "exchange") / args.steps
     # NVLink roofline of the inter-stage all-to-all (north_star): algorithmic
