@@ -1171,6 +1171,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       for (int e = 0; e < NE; e++)
         for (int i = 0; i < RB; i++)
           if ((e >> i) & 1) as[e] ^= sr[i];
+      if (sl.zfill_cap && p == 0) o << "      const unsigned zt = (unsigned)jt & zfill;\n";
       if (early && p == 0) {
         o << "      if (zmode) {\n";
         for (int e2 = 0; e2 < NE; e2++) o << "        v[" << e2 << "].x = 0; v[" << e2 << "].y = 0;\n";
@@ -1181,7 +1182,6 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
         // lazy zeros (zfill, launch argument: tile bits of active qubits
         // still |0>): an element with such a bit set is taken as zero --
         // the shard holds no zeros there, only what earlier runs left
-        o << "      const unsigned zt = (unsigned)jt & zfill;\n";
         for (int e = 0; e < NE; e++) {
           unsigned eb = 0;
           for (int i = 0; i < RB; i++)
@@ -1195,6 +1195,10 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
       if (early && p == 0) o << "      }\n";
     }
     if (early && ld && p == last) o << "      " << GS << "\n      " << next_issue << "\n";
+    // lazy zeros: a thread whose part of the tile index meets a still-zero
+    // qubit holds only zeros in the first phase, which every op keeps zero
+    const bool zskip_ops = sl.zfill_cap && p == 0;  // (zfill kernels never fold phase 0)
+    if (zskip_ops) o << "      if (zt == 0u) {\n";
     for (int oi = P.op_begin; oi < P.op_end; oi++) {
       const ShmOp &op = ops[oi];
       const double *c = coef + op.coef;
@@ -1444,6 +1448,7 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
         o << "      v[" << e << "].x *= " << lit(pend, f32) << "; v[" << e << "].y *= " << lit(pend, f32) << ";\n";
       pend = 1.0;
     }
+    if (zskip_ops) o << "      }\n";
     if (ld && p == last) {
       uint64_t limg[4] = {0, 0, 0, 0};
       for (int i = 0; i < RB; i++) limg[i] = sl.lcol[P.rbit[i]];
