@@ -277,8 +277,8 @@ atlas_status atlas_set_option_int(atlas_ctx *C, const char *key, int64_t v) {
     else if (k == "shm_const_pool") { o.shm_const_pool = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_autotune") { o.shm_autotune = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "async") { o.async = (int)v; replan = false; }
-    else if (k == "zero_lazy") { o.zero_lazy = (int)v; C->jit_ready = false; replan = false; }
-    else if (k == "zero_skip") { o.zero_skip = (int)v; C->jit_ready = false; replan = false; }
+    else if (k == "zero_lazy") { o.zero_lazy = (int)v; replan = false; }  // kernels compiled for a lazy chain run fine with zfill = 0
+    else if (k == "zero_skip") { o.zero_skip = (int)v; replan = false; }
     else if (k == "shm_tma") { o.shm_tma = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_fold_perm") { o.shm_fold_perm = (int)v; C->jit_ready = false; replan = false; }
     else if (k == "shm_addr_split") { o.shm_addr_split = (int)v; C->jit_ready = false; replan = false; }

@@ -28,6 +28,7 @@ struct Launch {
   void *jit_var[4] = {nullptr, nullptr, nullptr, nullptr};
   float tune_ms[4] = {-1.f, -1.f, -1.f, -1.f};
   int nvar = 0;
+  bool tune_warm = false;  // the first run after the JIT runs variant 0 untimed (cold pages, first launches)
 };
 
 // Exchange of one remap (stage boundary k-1 -> k): swap the g' top local

@@ -227,6 +227,7 @@ const int kDiagSel[11] = {0, 1, 2, 4, 8, 3, 5, 9, 6, 10, 12};
 
 int shm_nbuf_effective(int dtype, const ShmLaunch &sl);
 size_t shm_jit_smem(const std::string &src);
+void shm_jit_prime(void *jit);
 
 // TMA tile loads (option shm_tma, fp64 pipe kernels).  The shard is viewed
 // as a tensor of at most 5 dimensions, each a run of consecutive local slots
@@ -1720,6 +1721,7 @@ void shm_jit_prepare(atlas_ctx *C) {
     for (auto &ln : P)
       if (ln.type == L_SHM) {
         ln.nvar = 0;
+        ln.tune_warm = false;
         for (int v = 0; v < 4; v++) {
           ln.jit_var[v] = nullptr;
           ln.tune_ms[v] = -1.f;
@@ -1744,6 +1746,10 @@ void shm_jit_prepare(atlas_ctx *C) {
         ln.jit = ln.jit_var[0];
         if (ln.nvar < 2) ln.nvar = 0;  // nothing to tune
       }
+  // load every kernel now (dynamic shared-memory limit, occupancy): a
+  // first launch that loads its module stalls the stream and would count
+  // against its variant in the tuning runs
+  for (size_t i = 0; i < ents.size(); i++) shm_jit_prime(ents[i]);
 }
 
 static int g_nsms = 0;
@@ -1751,21 +1757,36 @@ static std::mutex g_tmap_mu;
 
 bool shm_jit_zero_ok(const void *jit) { return jit && ((const JitEntry *)jit)->zero_ok; }
 
+// Set the kernel's dynamic shared-memory limit and read its occupancy (once
+// per kernel; this also loads the module).
+static cudaError_t jit_prime(JitEntry *E, int NT) {
+  if (E->attr_set >= E->smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute((const void *)E->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, E->smem);
+  if (e != cudaSuccess) return e;
+  E->attr_set = E->smem;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)E->kern, NT, E->smem);
+  if (e != cudaSuccess) return e;
+  E->nt = occ < 1 ? 1 : occ;
+  return cudaSuccess;
+}
+void shm_jit_prime(void *jit) {
+  JitEntry *E = (JitEntry *)jit;
+  if (E && E->threads > 0) {
+    cudaError_t e = jit_prime(E, E->threads);
+    if (e != cudaSuccess) fail(ATLAS_E_CUDA, "shm_jit prime: %s", cudaGetErrorString(e));
+  }
+}
+
 // skip: non-active slots whose tiles with a 1 there are zero in and out (the
 // launch runs in place); those tiles are not visited at all
 cudaError_t launch_shm_jit(void *jit, void *st, void *dst, const ShmLaunch &sl, cudaStream_t s, int zmode,
                            uint64_t skip, void *const *peers, uint64_t zq) {
   JitEntry *E = (JitEntry *)jit;
   const int NT = E->threads > 0 ? E->threads : 1 << (sl.K - sl.RB);
-  if (E->attr_set < E->smem) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)E->kern,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, E->smem);
+  {
+    cudaError_t e = jit_prime(E, NT);
     if (e != cudaSuccess) return e;
-    E->attr_set = E->smem;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)E->kern, NT, E->smem);
-    if (e != cudaSuccess) return e;
-    E->nt = occ < 1 ? 1 : occ;
   }
   if (!g_nsms) {
     int dev = 0;
