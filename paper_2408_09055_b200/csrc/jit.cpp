@@ -379,7 +379,6 @@ static std::string shm_jit_source_body(const atlas_ctx *C, const ShmLaunch &sl, 
   const int K = sl.K, RB = sl.RB, NT = 1 << (K - RB), NE = 1 << RB, TILE = 1 << K;
   const int nbuf = shm_nbuf_effective(f32 ? 1 : 0, sl);
   const int esz = f32 ? 8 : 16;
-  auto swz = [&](int j) { return f32 ? swz_c64(j) : swz_c128(j); };
   const ShmOp *ops = C->ops.data() + sl.ops_off;
   const double *coef = C->coef.data() + sl.coef_off;
   const ShmPhase *ph = C->phases.data() + sl.phase_off;
